@@ -1,0 +1,367 @@
+#!/usr/bin/env python
+"""bench.py -- NUFFT points/s of the B200 hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2b] [--impl ours|reference]
+
+One STEP = one pass of the whole hot path over one batch of synthetic input
+(SURVEY.md §8a): setpts (fold + bin-sort), type-1 NUFFT (spread, FFT,
+truncate+deconvolve) and type-2 NUFFT (pre-correct+pad, FFT, interpolate).
+value = points of all ranks / device time per step (points/s), inputs resident
+in HBM; L2 is flushed (a 512 MB write) before every timed step, outside the
+timed events.  `e2e` is the same metric through the C ABI with pinned HOST
+buffers (H2D of x, y, z, c, fk and D2H of fk, c inside the timed region).
+
+Default workload = BASELINE.json configs[1] (C2b: fp32, 128^3 modes, 2^21
+uniform points, eps = 1e-6).  N > 1 (torchrun): every rank runs an independent
+replica of the workload with its own seed ("scaling": "weak", no data-path
+collective); the distributed slab path is reported separately once built.
+
+--impl reference: the CPU oracle (oracle/, plain C++ fp64) on the same config,
+rank 0 only, each step a bounded sample of the workload (2^19 points).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+CONFIGS = {
+    "c1": dict(name="C1", prec="f64", N=(32, 32, 32), Np=100_000, eps=1e-6, kind="uniform"),
+    "c2a": dict(name="C2a", prec="f32", N=(128, 128, 128), Np=1 << 21, eps=1e-4, kind="uniform"),
+    "c2b": dict(name="C2b", prec="f32", N=(128, 128, 128), Np=1 << 21, eps=1e-6, kind="uniform"),
+    "c3": dict(name="C3", prec="f64", N=(256, 256, 256), Np=8 * 256 ** 3, eps=1e-6,
+               kind="uniform"),
+    "c3e4": dict(name="C3", prec="f64", N=(256, 256, 256), Np=8 * 256 ** 3, eps=1e-4,
+                 kind="uniform"),
+}
+OUR_KERNELS_PER_STEP = 9  # bin_count, 3 scan, scatter | spread, truncate_deconv | pad, interp
+REF_SAMPLE = 1 << 19
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 50 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+        time.sleep(0.3)
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.1)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], [], set()
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, r[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def make_inputs(cfg, rank, device):
+    import synthetic
+    rdt = torch.float64 if cfg["prec"] == "f64" else torch.float32
+    cdt = torch.complex128 if cfg["prec"] == "f64" else torch.complex64
+    Np = cfg["Np"]
+    seed_shift = 1000 * rank
+    if cfg["kind"] == "landau":
+        pts = synthetic.landau_points(Np, seed=1 + seed_shift, device=device, dtype=rdt)
+    else:
+        pts = synthetic.uniform_points(Np, seed=1 + seed_shift, device=device, dtype=rdt)
+    c = synthetic.strengths(Np, seed=2 + seed_shift, device=device, dtype=cdt)
+    fk = synthetic.modes(*cfg["N"], seed=3 + seed_shift, device=device, dtype=cdt)
+    return pts, c, fk
+
+
+def algorithmic_bytes(cfg, stage):
+    """spread / interp move perm (4 B) + 3 coordinates + one strength
+    per point and the fine grid once: Np (4 + 5 r) + nf^3 2 r bytes per launch."""
+    r = 8 if cfg["prec"] == "f64" else 4
+    nf3 = 8 * cfg["N"][0] * cfg["N"][1] * cfg["N"][2]
+    if stage in ("spread", "interp"):
+        return cfg["Np"] * (4 + 5 * r) + nf3 * 2 * r
+    raise ValueError(stage)
+
+
+def load_traffic(cfg_key, kernel):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)[cfg_key][kernel]
+    except Exception:
+        return None
+
+
+def run_ours(args, cfg):
+    import paper_2605_10678_b200 as nb
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    stream = torch.cuda.current_stream(device)
+
+    pts, c, fk = make_inputs(cfg, rank, device)
+    N, Np = cfg["N"], cfg["Np"]
+    plan = nb.Plan(N, cfg["eps"], precision=cfg["prec"], timing=True, device=device)
+    c2 = torch.empty(Np, dtype=c.dtype, device=device)
+    fk_out = torch.empty_like(fk)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=device)
+
+    def step():
+        plan.setpts(*pts)
+        plan.type1(c, out=fk_out)
+        plan.type2(fk, out=c2)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    stage = {k: [] for k in ("ms_setpts", "ms_spread", "ms_fft", "ms_deconv", "ms_pad",
+                             "ms_interp")}
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        flush.fill_(k & 0xff)                      # evict L2 (outside the timed events)
+        evs[k][0].record(stream)
+        step()
+        evs[k][1].record(stream)
+        info = plan.info()                         # syncs; per-stage events of this step
+        for key in stage:
+            stage[key].append(info[key])
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    clocks = sampler.stop()
+    t_ms = sum(a.elapsed_time(b) for a, b in evs)
+    t_max = t_ms
+    if ws > 1:
+        t = torch.tensor([t_ms], device=device, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t_max = float(t.item())
+    ms_per_step = t_max / args.steps
+    value = ws * Np / (ms_per_step / 1e3)
+
+    # -- end to end through the C ABI with pinned host buffers
+    hp = [p.cpu().pin_memory() for p in pts]
+    hc = c.cpu().pin_memory()
+    hfk = fk.cpu().pin_memory()
+    hfk_out = torch.empty(fk.shape, dtype=fk.dtype).pin_memory()
+    hc2 = torch.empty(Np, dtype=c.dtype).pin_memory()
+
+    def e2e_step():
+        plan.setpts(*hp)
+        plan.type1(hc, out=hfk_out)
+        plan.type2(hfk, out=hc2)
+
+    e2e_steps = max(3, min(args.steps, 20))
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    te = e0.elapsed_time(e1)
+    if ws > 1:
+        t = torch.tensor([te], device=device, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        te = float(t.item())
+    r = 8 if cfg["prec"] == "f64" else 4
+    nmodes = N[0] * N[1] * N[2]
+    h2d = 3 * Np * r + Np * 2 * r + nmodes * 2 * r
+    d2h = nmodes * 2 * r + Np * 2 * r
+
+    # -- roofline of the dominant kernel of ours (spread or interp)
+    med = {k: statistics.median(v) for k, v in stage.items() if v and min(v) >= 0}
+    dom = "spread" if med.get("ms_spread", 0) >= med.get("ms_interp", 0) else "interp"
+    dom_ms = med["ms_" + dom]
+    hbm, peak_src = peaks()
+    bytes_alg = algorithmic_bytes(cfg, dom)
+    achieved = bytes_alg / (dom_ms / 1e3) / 1e9
+    out = None
+    if rank == 0:
+        cpu = cpu_baseline(cfg) if (ws == 1 and not args.no_cpu_baseline) else None
+        out = {
+            "metric": "NUFFT points/s (setpts + type-1 spread + type-2 interp per point)",
+            "value": value, "unit": "points/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64" if cfg["prec"] == "f64" else "f32", "data": "synthetic",
+            "config": {"workload": f"{cfg['name']}: {cfg['prec']} {N[0]}x{N[1]}x{N[2]} modes, "
+                                   f"{Np} {cfg['kind']} points, eps={cfg['eps']:g}",
+                       "N": list(N), "Np_per_gpu": Np, "eps": cfg["eps"], "w": plan.info()["w"],
+                       "precision": cfg["prec"], "points": cfg["kind"],
+                       "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU",
+                       "l2": "flushed (512 MB write) before every timed step"},
+            "stage_ms_median": med,
+            "e2e": {"value": ws * Np / (te / e2e_steps / 1e3), "unit": "points/s",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": te / e2e_steps},
+            "gpu_launches": OUR_KERNELS_PER_STEP * args.steps,
+            "roofline": {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": hbm,
+                         "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm,
+                         "traffic": load_traffic(args.config, dom),
+                         "algorithmic_bytes_per_launch": bytes_alg, "ms_per_launch": dom_ms},
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+        }
+    plan.close()
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return out
+
+
+def cpu_baseline(cfg, sample=REF_SAMPLE):
+    """The oracle as it stands, on a bounded sample of the workload, all host cores."""
+    import oracle
+    import synthetic
+    t0 = time.perf_counter()
+    x, y, z = (v.numpy() for v in synthetic.uniform_points(sample))
+    c = synthetic.strengths(sample).numpy()
+    fk = synthetic.modes(*cfg["N"]).numpy()
+    t_gen = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    oracle.type1(x, y, z, c, cfg["N"], cfg["eps"])
+    oracle.type2(x, y, z, fk, cfg["eps"])
+    t = time.perf_counter() - t0
+    return {"value": sample / t, "unit": "points/s", "cores": oracle.num_threads(),
+            "kind": "oracle",
+            "sample": f"{sample} uniform points of the {cfg['name']} workload ({cfg['N'][0]}^3 "
+                      f"modes, eps={cfg['eps']:g}), one type-1 + one type-2 in fp64",
+            "seconds": t, "input_gen_seconds": t_gen}
+
+
+def run_reference(args, cfg):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return None
+    import oracle
+    import synthetic
+    sample = REF_SAMPLE
+    x, y, z = (v.numpy() for v in synthetic.uniform_points(sample))
+    c = synthetic.strengths(sample).numpy()
+    fk = synthetic.modes(*cfg["N"]).numpy()
+
+    def step():
+        oracle.type1(x, y, z, c, cfg["N"], cfg["eps"])
+        oracle.type2(x, y, z, fk, cfg["eps"])
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    t = (time.perf_counter() - t0) / args.steps
+    v = sample / t
+    N = cfg["N"]
+    return {
+        "impl": "reference", "metric": "NUFFT points/s (setpts + type-1 spread + type-2 interp per point)",
+        "value": v, "unit": "points/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg['name']}: {cfg['prec']} {N[0]}x{N[1]}x{N[2]} modes, "
+                               f"{cfg['Np']} {cfg['kind']} points, eps={cfg['eps']:g}",
+                   "sample_points": sample},
+        "cpu_baseline": {"value": v, "unit": "points/s", "cores": oracle.num_threads(),
+                         "kind": "oracle",
+                         "sample": f"{sample} points of the workload per step (oracle type-1 + type-2, fp64)"},
+        "e2e": {"value": v, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2b", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    out = run_reference(args, cfg) if args.impl == "reference" else run_ours(args, cfg)
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

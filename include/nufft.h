@@ -1,0 +1,151 @@
+/*
+ * nufft.h -- C ABI of libnufft.so, the B200-native (sm_100a) hot path of the
+ * distributed 3D NUFFT of arXiv 2605.10678.
+ *
+ * The problem (§2, Eq. 1-2), points x_j in [0, L)^3, N_d even,
+ * modes n in {-N_d/2 .. N_d/2-1}:
+ *   type 1:  fk[n] = sum_j c_j exp(iflag * i (2 pi / L) n . x_j)
+ *   type 2:  c_j   = sum_n fk[n] exp(-iflag * i (2 pi / L) n . x_j)
+ * With iflag = -1 these are exactly Eq. (1) and Eq. (2) and the pair is adjoint
+ * (PAPER.md:95, 123).  The library evaluates them by the paper's factorisation
+ *   type 1 = D chi F C   (Eq. 3)
+ *   type 2 = C^T F^-1 chi^T D   (Eq. 4)
+ * with the ES window, sigma = 2 (fine grid nf_d = 2 N_d,
+ * PAPER.md:141, 181) and w chosen from eps (reading R1).
+ *
+ * Conventions common to all calls
+ * -------------------------------
+ * Pointers.  Every array argument may be DEVICE memory (cudaMalloc / torch CUDA
+ *   tensor) or HOST memory (pinned or pageable).  Host arrays are staged through
+ *   plan-owned device buffers with cudaMemcpyAsync on the plan stream; when an
+ *   OUTPUT is host memory the call returns only after the result is in it.  With
+ *   device arrays every call is asynchronous (stream-ordered on opts.stream).
+ * Layout.  Complex values are interleaved (re, im) pairs of the plan precision
+ *   (float2 / double2 = torch.complex64 / complex128).  Coordinates are three
+ *   separate real arrays (SoA) of the plan precision.  Mode arrays are
+ *   N1 x N2 x N3 with x fastest: flat index (n1+N1/2) + N1 ((n2+N2/2) + N2 (n3+N3/2))
+ *   for modeord 0 (centered, default); for modeord 1 (FFT order) index i_d holds
+ *   n_d = i_d for i_d < N_d/2 and i_d - N_d otherwise.  Fine grids (nufft_spread /
+ *   nufft_interp) are nf1 x nf2 x nf3 complex, x fastest, nf_d = 2 N_d.
+ * Ownership.  The caller owns every array it passes and the stream.  setpts
+ *   COPIES what it needs (sorted point records), so x, y, z may be reused once the
+ *   stream has passed the call.  The plan owns its fine grid, bins, tables, cuFFT
+ *   plan and staging buffers; nufft_destroy frees them.
+ * Errors.  Every call returns an int status: 0 = NUFFT_OK, 1 = a warning
+ *   (NUFFT_WARN_EPS_CLAMPED), >= 2 an error (enum below; nufft_strerror names it).
+ *   No exception or exit() crosses the ABI.  Asynchronous CUDA faults surface as
+ *   NUFFT_ERR_CUDA at a later call.  A handle is not re-entrant; distinct handles
+ *   on distinct streams are independent.
+ */
+#ifndef NUFFT_B200_H
+#define NUFFT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct nufft_plan_s* nufft_handle;
+
+enum { NUFFT_F32 = 0, NUFFT_F64 = 1 };
+
+enum {
+    NUFFT_OK = 0,
+    NUFFT_WARN_EPS_CLAMPED = 1, /* eps outside [1e-15, 1e-1] (fp64) / [1e-7, 1e-1] (fp32): clamped */
+    NUFFT_ERR_ARG = 2,          /* null handle / pointer, bad enum, bad option                      */
+    NUFFT_ERR_MODES = 3,        /* some N_d odd, < 2, or 2 N_d < w                                   */
+    NUFFT_ERR_NPTS = 4,         /* Np < 0 or Np >= 2^31 on one GPU                                  */
+    NUFFT_ERR_NOT_SET = 5,      /* execute / spread / interp before setpts                           */
+    NUFFT_ERR_ALLOC = 6,        /* device allocation failed                                          */
+    NUFFT_ERR_CUDA = 7,         /* a CUDA runtime error (launch, copy, or an earlier async fault)    */
+    NUFFT_ERR_CUFFT = 8,        /* cuFFT plan / exec failure                                         */
+    NUFFT_ERR_NCCL = 9,         /* NCCL failure (distributed plans)                                  */
+    NUFFT_ERR_UNSUPPORTED = 10  /* option combination not built                                      */
+};
+
+typedef struct {
+    double L;          /* period of the torus [0, L)^3; default 2 pi                   */
+    int modeord;       /* 0 = centered modes (default), 1 = FFT order                                 */
+    void* stream;      /* cudaStream_t for every call of the plan; NULL = the legacy default stream */
+    void* comm;        /* NULL = single GPU; else a communicator from nufft_comm_init (slab mode)    */
+    int points_owned;  /* distributed: 1 = caller guarantees each point lies in this rank's z-slab   */
+    int tile[3];       /* bin / tile edge in fine cells per axis; 0 = built-in table by w            */
+    int timing;        /* 1 = record per-stage CUDA events (read back by nufft_get_info)              */
+    int reserved[7];
+} nufft_opts;
+
+typedef struct {
+    int precision;          /* NUFFT_F32 / NUFFT_F64                                  */
+    int w;                  /* ES kernel width (cells)                                */
+    double beta;            /* ES shape parameter                                     */
+    double eps;             /* tolerance after clamping                               */
+    int64_t N[3];           /* modes per axis                                         */
+    int64_t nf[3];          /* fine grid per axis (= 2 N)                             */
+    int tile[3];            /* bin edge per axis                                      */
+    int64_t nbins;          /* number of bins                                         */
+    int64_t Np;             /* points after setpts (this rank)                        */
+    size_t device_bytes;    /* device memory owned by the plan                        */
+    int nranks, rank;       /* 1, 0 on a single GPU                                   */
+    int64_t slab_lo, slab_hi; /* fine z-planes owned by this rank                     */
+    /* per-stage device milliseconds of the most recent calls (opts.timing = 1), else -1 */
+    float ms_setpts, ms_spread, ms_fold, ms_fft, ms_deconv, ms_pad, ms_interp, ms_comm;
+} nufft_info;
+
+/* Fills *o with the defaults (L = 2 pi, centered modes, default stream, single GPU). */
+int nufft_default_opts(nufft_opts* o);
+
+/* Create a plan (all precomputation "once during initialization").
+ * N1, N2, N3: modes per axis (even, >= 2, 2 N_d >= w).  iflag: sign of the type-1
+ * exponent (-1 reproduces Eq. 1); type 2 uses -iflag.  eps: requested relative
+ * l2 tolerance.  precision: NUFFT_F32 or NUFFT_F64.  opts may be NULL (defaults).
+ * Host: computes w, beta, the deconvolution factors p_d(n) = 2 / (w phihat(pi n w / nf_d))
+ * by Gauss-Legendre quadrature, allocates the fine grid and the cuFFT plan.
+ * Blocks the host.  On success *out is a new handle. */
+int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int precision,
+               const nufft_opts* opts, nufft_handle* out);
+
+/* Set the nonuniform points: fold onto [0, L)^3, bin-sort
+ * them by tile (counting sort with warp-level prefix scans), store sorted per-point
+ * stencil records.  x, y, z: Np reals each of the plan precision, device or host.
+ * Distributed plans: collective over the communicator; points are redistributed
+ * to their owning z-slab unless opts.points_owned (blocks the host for the counts). */
+int nufft_setpts(nufft_handle h, int64_t Np, const void* x, const void* y, const void* z);
+
+/* Type-1 NUFFT (Eq. 3): c = Np complex strengths (caller order), fk = N1 N2 N3 complex out.
+ * Spread (C) -> FFT with sign iflag (F) -> truncate (chi) + deconvolve (D), fused. */
+int nufft_execute_type1(nufft_handle h, const void* c, void* fk);
+
+/* Type-2 NUFFT (Eq. 4): fk = N1 N2 N3 complex in, c = Np complex out in caller order.
+ * Pre-correct (D) + zero-pad (chi^T), fused -> FFT with sign -iflag -> interpolate (C^T). */
+int nufft_execute_type2(nufft_handle h, const void* fk, void* c);
+
+/* The spreading operator alone (Step 1): grid = C c on the periodic
+ * nf1 x nf2 x nf3 fine grid (overwritten).  Single-GPU plans only. */
+int nufft_spread(nufft_handle h, const void* c, void* grid);
+
+/* The interpolation operator alone (C^T): c = C^T grid, caller order. */
+int nufft_interp(nufft_handle h, const void* grid, void* c);
+
+/* Free everything the plan owns.  Accepts NULL. */
+int nufft_destroy(nufft_handle h);
+
+/* Plan parameters and, with opts.timing, the last per-stage device times.  Blocks. */
+int nufft_get_info(nufft_handle h, nufft_info* info);
+
+/* Static string for a status code (host). */
+const char* nufft_strerror(int code);
+
+/* ---- multi-GPU bootstrap (one process per GPU; slab decomposition along z) ----
+ * PyTorch only carries the 128-byte id through its process group. */
+int nufft_comm_unique_id(char id[128]);                                    /* rank 0, host */
+int nufft_comm_init(const char id[128], int nranks, int rank, void** comm); /* collective   */
+int nufft_comm_destroy(void* comm);
+/* Distributed mode layout: this rank's [lo, hi) range of centered mode indices per axis. */
+int nufft_local_modes(nufft_handle h, int64_t lo[3], int64_t hi[3]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NUFFT_B200_H */

@@ -458,11 +458,11 @@ int orc_type2(int64_t Np, const double* x, const double* y, const double* z, con
  * directly with cos/sin (no recurrence).  If sel != NULL only the nsel modes with
  * flat indices sel[k] are evaluated, into fk_out[k]; else all N1 N2 N3 modes.
  * ------------------------------------------------------------------------- */
-static void phase_table(int64_t Np, const double* x, int64_t N, int iflag, double L,
+static void phase_table(int64_t n, const double* x, int64_t N, int iflag, double L,
                         std::vector<cplx>& e) {
-    e.resize((size_t)(Np * N));
+    e.resize((size_t)(n * N));
 #pragma omp parallel for schedule(static)
-    for (int64_t j = 0; j < Np; ++j)
+    for (int64_t j = 0; j < n; ++j)
         for (int64_t i = 0; i < N; ++i) {
             double ang = (double)iflag * (2.0 * kPi / L) * (double)(i - N / 2) * x[j];
             e[(size_t)(j * N + i)] = cplx(std::cos(ang), std::sin(ang));
@@ -475,20 +475,26 @@ void orc_nudft1(int64_t Np, const double* x, const double* y, const double* z,
     const cplx* cc = reinterpret_cast<const cplx*>(c);
     cplx* fk = reinterpret_cast<cplx*>(fk_out);
     int sgn = iflag >= 0 ? 1 : -1;
-    std::vector<cplx> e1, e2, e3;
-    phase_table(Np, x, N1, sgn, L, e1);
-    phase_table(Np, y, N2, sgn, L, e2);
-    phase_table(Np, z, N3, sgn, L, e3);
     int64_t nout = sel ? nsel : N1 * N2 * N3;
+    for (int64_t k = 0; k < nout; ++k) fk[k] = cplx(0.0, 0.0);
+    /* points in chunks so the phase tables stay small; sum over j in index order */
+    const int64_t chunk = 16384;
+    std::vector<cplx> e1, e2, e3;
+    for (int64_t j0 = 0; j0 < Np; j0 += chunk) {
+        int64_t n = Np - j0 < chunk ? Np - j0 : chunk;
+        phase_table(n, x + j0, N1, sgn, L, e1);
+        phase_table(n, y + j0, N2, sgn, L, e2);
+        phase_table(n, z + j0, N3, sgn, L, e3);
 #pragma omp parallel for schedule(dynamic, 16)
-    for (int64_t k = 0; k < nout; ++k) {
-        int64_t flat = sel ? sel[k] : k;
-        int64_t i1 = flat % N1, i2 = (flat / N1) % N2, i3 = flat / (N1 * N2);
-        cplx acc(0.0, 0.0);
-        for (int64_t j = 0; j < Np; ++j)
-            acc += cc[j] * e1[(size_t)(j * N1 + i1)] * e2[(size_t)(j * N2 + i2)] *
-                   e3[(size_t)(j * N3 + i3)];
-        fk[k] = acc;
+        for (int64_t k = 0; k < nout; ++k) {
+            int64_t flat = sel ? sel[k] : k;
+            int64_t i1 = flat % N1, i2 = (flat / N1) % N2, i3 = flat / (N1 * N2);
+            cplx acc(0.0, 0.0);
+            for (int64_t j = 0; j < n; ++j)
+                acc += cc[j0 + j] * e1[(size_t)(j * N1 + i1)] * e2[(size_t)(j * N2 + i2)] *
+                       e3[(size_t)(j * N3 + i3)];
+            fk[k] += acc;
+        }
     }
 }
 

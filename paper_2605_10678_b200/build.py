@@ -1,0 +1,106 @@
+"""Build libnufft.so in-tree with nvcc for sm_100a (no JIT cache, no torch extension).
+
+    python -m paper_2605_10678_b200.build [--force] [-j N]
+
+Every CUDA translation unit is compiled with
+``-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo``; the host orchestration
+(plan.cpp) with the same nvcc driver; the result is linked with cuFFT into
+``paper_2605_10678_b200/libnufft.so`` next to this file.
+"""
+from __future__ import annotations
+
+import argparse
+import concurrent.futures as cf
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+ROOT = os.path.dirname(HERE)
+BUILD = os.path.join(HERE, "_build")
+LIB = os.path.join(HERE, "libnufft.so")
+CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+NVCC = os.path.join(CUDA, "bin", "nvcc")
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
+          "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+CU_FLAGS = ARCH + COMMON + ["--expt-relaxed-constexpr", "-Xptxas", "-v"]
+
+SOURCES = ["sort.cu", "spread.cu", "interp.cu", "elementwise.cu", "plan.cpp"]
+
+
+def _nccl_dirs():
+    try:
+        import nvidia.nccl as nn  # torch's NCCL wheel (2.28.x)
+        base = list(nn.__path__)[0]
+        inc, lib = os.path.join(base, "include"), os.path.join(base, "lib")
+        if os.path.exists(os.path.join(inc, "nccl.h")):
+            return inc, lib
+    except Exception:
+        pass
+    return None, None
+
+
+def _deps(src):
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
+    headers.append(os.path.join(ROOT, "include", "nufft.h"))
+    return [os.path.join(CSRC, src)] + headers
+
+
+def _stale(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
+
+
+def _compile(src, force, log):
+    obj = os.path.join(BUILD, src + ".o")
+    if not force and not _stale(obj, _deps(src)):
+        return obj, ""
+    flags = list(CU_FLAGS) if src.endswith(".cu") else ARCH + COMMON
+    cmd = [NVCC] + flags + ["-c", os.path.join(CSRC, src), "-o", obj]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
+    out = r.stdout + r.stderr
+    if log:
+        with open(os.path.join(BUILD, src + ".ptxas.txt"), "w") as f:
+            f.write(out)
+    return obj, out
+
+
+def build(force: bool = False, jobs: int = 8, verbose: bool = False) -> str:
+    os.makedirs(BUILD, exist_ok=True)
+    with cf.ThreadPoolExecutor(max_workers=jobs) as ex:
+        futs = {ex.submit(_compile, s, force, True): s for s in SOURCES}
+        objs = {}
+        for f in cf.as_completed(futs):
+            obj, out = f.result()
+            objs[futs[f]] = obj
+            if verbose and out:
+                print(out)
+    objs = [objs[s] for s in SOURCES]
+    if force or _stale(LIB, objs):
+        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB + ".tmp"] + objs + \
+            ["-lcufft", "-Xlinker", "-rpath," + os.path.join(CUDA, "lib64")]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+        os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("-j", type=int, default=8)
+    ap.add_argument("-v", action="store_true")
+    a = ap.parse_args()
+    print(build(a.force, a.j, a.v))
+
+
+if __name__ == "__main__":
+    sys.exit(main())

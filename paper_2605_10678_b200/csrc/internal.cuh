@@ -1,0 +1,82 @@
+// internal.cuh -- shared internals of libnufft.so (the CUDA product path).
+// Nothing here is visible through the C ABI (include/nufft.h).  The CPU oracle
+// (oracle/) shares none of this code.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cufft.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "../../include/nufft.h"
+
+namespace nufft {
+
+// ---------------------------------------------------------------- complex types
+template <typename T> struct Cx;
+template <> struct Cx<float> { using type = float2; };
+template <> struct Cx<double> { using type = double2; };
+
+// ---------------------------------------------------------------- geometry
+// Fine grid, bins and the fold/rescale map shared by all point kernels.
+struct Geom {
+    int64_t nf[3];      // fine grid cells per axis (nf = 2 N)
+    int T[3];           // bin / tile edge (fine cells)
+    int nb[3];          // bins per axis = ceil(nf / T)
+    int64_t z_lo;       // first fine z-plane owned by this rank (0 on one GPU)
+    int64_t nz_loc;     // fine z-planes owned by this rank (nf[2] on one GPU)
+    double L;           // period
+    double scale[3];    // nf / L
+    int w;              // kernel width
+};
+
+// Sorted point records written by setpts (SoA, indexed by sorted slot).
+//   perm[i]  : original (caller) index of the point in slot i
+//   d{x,y,z} : ls - la, the stencil phase offset in cells, in [w/2 - 1, w/2]
+//   la[i]    : packed bin-local stencil base (8 bits per axis), la in [0, T]
+// The weight of stencil node k on axis d is phi(2 (k - d_d) / w).
+template <typename T> struct PtsView {
+    const uint32_t* offset;  // nbins + 1 bin starts (exclusive scan of counts)
+    const uint32_t* perm;
+    const T* dx;
+    const T* dy;
+    const T* dz;
+    const uint32_t* la;
+};
+
+// ---------------------------------------------------------------- kernel launchers
+// sort.cu
+template <typename T>
+cudaError_t launch_bin_sort(const Geom& g, int64_t Np, const T* x, const T* y, const T* z,
+                            uint32_t* count, uint32_t* offset, uint32_t* blocksum,
+                            uint32_t* bin_of, uint32_t* rank_of, uint32_t* perm, T* dx, T* dy,
+                            T* dz, uint32_t* la, int64_t nbins, cudaStream_t s);
+size_t scan_blocksum_elems(int64_t nbins);
+
+// spread.cu: grid (nf[0] x nf[1] x nz_loc complex, x fastest) += C c
+template <typename T>
+cudaError_t launch_spread(const Geom& g, const PtsView<T>& p, int64_t nbins,
+                          const typename Cx<T>::type* c, typename Cx<T>::type* grid, double beta,
+                          cudaStream_t s);
+// interp.cu: c = C^T grid
+template <typename T>
+cudaError_t launch_interp(const Geom& g, const PtsView<T>& p, int64_t nbins,
+                          const typename Cx<T>::type* grid, typename Cx<T>::type* c, double beta,
+                          cudaStream_t s);
+// elementwise.cu
+template <typename T>
+cudaError_t launch_truncate_deconv(const typename Cx<T>::type* grid, const int64_t nf[3],
+                                   const int64_t N[3], const T* p1, const T* p2, const T* p3,
+                                   int modeord, typename Cx<T>::type* fk, cudaStream_t s);
+template <typename T>
+cudaError_t launch_pad_precorrect(const typename Cx<T>::type* fk, const int64_t N[3],
+                                  const T* p1, const T* p2, const T* p3, int modeord,
+                                  const int64_t nf[3], typename Cx<T>::type* grid,
+                                  cudaStream_t s);
+
+// host-side window helpers (plan.cu)
+int select_width(double eps, int precision, int* w, double* beta, double* eps_used);
+double es_phihat(double xi, double beta);
+
+}  // namespace nufft

@@ -1,0 +1,651 @@
+// plan.cpp -- the C ABI of libnufft.so (include/nufft.h): plan, setpts,
+// execute type 1 / type 2, spread / interp, destroy, info.
+//
+// Host-side orchestration only: parameter choice, the deconvolution table by
+// Gauss-Legendre quadrature (once per plan), device buffers,
+// the cuFFT plan, host<->device staging, CUDA-event stage timing.  Every step
+// of the NUFFT itself runs in the kernels of sort.cu / spread.cu / interp.cu /
+// elementwise.cu (and cuFFT for the uniform FFT).
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "internal.cuh"
+
+using namespace nufft;
+
+namespace nufft {
+
+// Width rule (reading R1; PAPER.md:181 defers to Barnett 2019):
+// w = ceil(log10(1/eps)) + 1 clamped to [2, 16], beta = 2.30 w, sigma = 2.
+// fp32 plans clamp eps to >= 1e-7 (single precision cannot resolve less).
+int select_width(double eps, int precision, int* w, double* beta, double* eps_used) {
+    int st = NUFFT_OK;
+    const double lo = precision == NUFFT_F32 ? 1e-7 : 1e-15;
+    if (!(eps >= lo)) {
+        eps = lo;
+        st = NUFFT_WARN_EPS_CLAMPED;
+    }
+    if (eps > 1e-1) {
+        eps = 1e-1;
+        st = NUFFT_WARN_EPS_CLAMPED;
+    }
+    int ww = (int)std::ceil(std::log10(1.0 / eps)) + 1;
+    ww = ww < 2 ? 2 : (ww > 16 ? 16 : ww);
+    *w = ww;
+    *beta = 2.30 * (double)ww;
+    *eps_used = eps;
+    return st;
+}
+
+// phihat(xi) = int_{-1}^{1} exp(beta (sqrt(1 - z^2) - 1)) cos(xi z) dz
+// (PAPER.md:178-179), evaluated on theta = asin(z) with a 100-node
+// Gauss-Legendre rule whose nodes come from std::legendre + Newton.
+double es_phihat(double xi, double beta) {
+    static std::vector<double> nodes, weights;
+    const int n = 100;
+    if (nodes.empty()) {
+        nodes.resize(n);
+        weights.resize(n);
+        for (int k = 0; k < n; ++k) {
+            double t = std::cos(M_PI * (k + 0.75) / (n + 0.5));
+            double dp = 1.0;
+            for (int it = 0; it < 50; ++it) {
+                const double pn = std::legendre(n, t), pm = std::legendre(n - 1, t);
+                dp = n * (pm - t * pn) / (1.0 - t * t);
+                const double step = pn / dp;
+                t -= step;
+                if (std::fabs(step) < 1e-16) break;
+            }
+            const double pn = std::legendre(n, t), pm = std::legendre(n - 1, t);
+            dp = n * (pm - t * pn) / (1.0 - t * t);
+            nodes[k] = t;
+            weights[k] = 2.0 / ((1.0 - t * t) * dp * dp);
+        }
+    }
+    const double h = 0.5 * M_PI;
+    double acc = 0.0;
+    for (int k = 0; k < n; ++k) {
+        const double th = h * nodes[k];
+        const double ct = std::cos(th);
+        acc += weights[k] * std::exp(beta * (ct - 1.0)) * std::cos(xi * std::sin(th)) * ct;
+    }
+    return h * acc;
+}
+
+}  // namespace nufft
+
+struct nufft_plan_s {
+    int prec = NUFFT_F64;
+    int iflag = -1;
+    double eps = 0;
+    int w = 0;
+    double beta = 0;
+    int modeord = 0;
+    int64_t N[3] = {0, 0, 0};
+    int64_t nf[3] = {0, 0, 0};
+    Geom geom{};
+    int64_t nbins = 0;
+    cudaStream_t stream = nullptr;
+    size_t real_size = 8;
+    size_t cplx_size = 16;
+
+    void* d_p[3] = {nullptr, nullptr, nullptr};  // deconvolution factors, precision type
+    void* d_grid = nullptr;                      // nf1 nf2 nf3 complex
+    size_t grid_bytes = 0;
+    cufftHandle fft = 0;
+    bool fft_ok = false;
+
+    // points
+    int64_t Np = -1;
+    int64_t cap = 0;
+    uint32_t* count = nullptr;
+    uint32_t* offset = nullptr;
+    uint32_t* blocksum = nullptr;
+    uint32_t* bin_of = nullptr;
+    uint32_t* rank_of = nullptr;
+    uint32_t* perm = nullptr;
+    uint32_t* la = nullptr;
+    void* dx = nullptr;
+    void* dy = nullptr;
+    void* dz = nullptr;
+
+    // host staging
+    void* stage_in = nullptr;
+    size_t stage_in_bytes = 0;
+    void* stage_out = nullptr;
+    size_t stage_out_bytes = 0;
+
+    // timing
+    bool timing = false;
+    cudaEvent_t ev0[8] = {};
+    cudaEvent_t ev[8] = {};
+    bool ev_used[8] = {};
+
+    size_t bytes = 0;
+};
+
+namespace {
+
+enum { EV_SETPTS = 0, EV_SPREAD, EV_FFT, EV_DECONV, EV_PAD, EV_INTERP };
+
+struct StageTimer {
+    nufft_plan_s* p;
+    int id;
+    StageTimer(nufft_plan_s* pl, int i) : p(pl), id(i) {
+        if (p->timing) cudaEventRecord(p->ev0[id], p->stream);
+    }
+    ~StageTimer() {
+        if (p->timing) {
+            cudaEventRecord(p->ev[id], p->stream);
+            p->ev_used[id] = true;
+        }
+    }
+};
+
+int cuda_status(cudaError_t e) {
+    if (e == cudaSuccess) return NUFFT_OK;
+    if (e == cudaErrorMemoryAllocation) return NUFFT_ERR_ALLOC;
+    return NUFFT_ERR_CUDA;
+}
+
+#define CK(expr)                                  \
+    do {                                          \
+        cudaError_t e__ = (expr);                 \
+        if (e__ != cudaSuccess) return cuda_status(e__); \
+    } while (0)
+
+bool is_device_ptr(const void* ptr) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int dev_alloc(nufft_plan_s* p, void** ptr, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMalloc(ptr, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *ptr = nullptr;
+        return NUFFT_ERR_ALLOC;
+    }
+    p->bytes += bytes;
+    return NUFFT_OK;
+}
+
+void dev_free(nufft_plan_s* p, void** ptr, size_t bytes) {
+    if (*ptr) {
+        cudaFree(*ptr);
+        p->bytes -= bytes;
+        *ptr = nullptr;
+    }
+}
+
+// Device view of a caller array: device pointers pass through, host arrays are
+// copied into the plan's input staging buffer (offset `off` bytes into it).
+int input_view(nufft_plan_s* p, const void* src, size_t bytes, size_t off, size_t total,
+               const void** dev) {
+    if (bytes == 0 || is_device_ptr(src)) {
+        *dev = src;
+        return NUFFT_OK;
+    }
+    if (p->stage_in_bytes < total) {
+        dev_free(p, &p->stage_in, p->stage_in_bytes);
+        p->stage_in_bytes = 0;
+        int st = dev_alloc(p, &p->stage_in, total);
+        if (st) return st;
+        p->stage_in_bytes = total;
+    }
+    char* d = static_cast<char*>(p->stage_in) + off;
+    CK(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, p->stream));
+    *dev = d;
+    return NUFFT_OK;
+}
+
+int output_view(nufft_plan_s* p, void* dst, size_t bytes, void** dev, bool* staged) {
+    *staged = false;
+    if (bytes == 0 || is_device_ptr(dst)) {
+        *dev = dst;
+        return NUFFT_OK;
+    }
+    if (p->stage_out_bytes < bytes) {
+        dev_free(p, &p->stage_out, p->stage_out_bytes);
+        p->stage_out_bytes = 0;
+        int st = dev_alloc(p, &p->stage_out, bytes);
+        if (st) return st;
+        p->stage_out_bytes = bytes;
+    }
+    *dev = p->stage_out;
+    *staged = true;
+    return NUFFT_OK;
+}
+
+int finish_output(nufft_plan_s* p, void* dst, const void* dev, size_t bytes, bool staged) {
+    if (!staged) return NUFFT_OK;
+    CK(cudaMemcpyAsync(dst, dev, bytes, cudaMemcpyDeviceToHost, p->stream));
+    CK(cudaStreamSynchronize(p->stream));
+    return NUFFT_OK;
+}
+
+// Default bin edge by width: the (T + w)^3 subgrid of complex cells should stay
+// near 64 KB (fp64: T + w ~ 16, fp32: T + w ~ 20) so that two or more CTAs fit
+// per SM; never below 4 and never larger than the grid.
+int default_tile(int w, int prec, int64_t nf) {
+    const int edge = prec == NUFFT_F64 ? 16 : 20;
+    int t = edge - w;
+    if (t < 4) t = 4;
+    if (t > 64) t = 64;
+    if (t > nf) t = (int)nf;
+    return t;
+}
+
+template <typename T>
+PtsView<T> pts_view(nufft_plan_s* p) {
+    PtsView<T> v;
+    v.offset = p->offset;
+    v.perm = p->perm;
+    v.dx = static_cast<const T*>(p->dx);
+    v.dy = static_cast<const T*>(p->dy);
+    v.dz = static_cast<const T*>(p->dz);
+    v.la = p->la;
+    return v;
+}
+
+int do_spread(nufft_plan_s* p, const void* c_dev, void* grid_dev) {
+    CK(cudaMemsetAsync(grid_dev, 0, p->grid_bytes, p->stream));
+    StageTimer tm(p, EV_SPREAD);
+    if (p->prec == NUFFT_F64)
+        CK(launch_spread<double>(p->geom, pts_view<double>(p), p->nbins,
+                                 static_cast<const double2*>(c_dev),
+                                 static_cast<double2*>(grid_dev), p->beta, p->stream));
+    else
+        CK(launch_spread<float>(p->geom, pts_view<float>(p), p->nbins,
+                                static_cast<const float2*>(c_dev), static_cast<float2*>(grid_dev),
+                                p->beta, p->stream));
+    return NUFFT_OK;
+}
+
+int do_interp(nufft_plan_s* p, const void* grid_dev, void* c_dev) {
+    StageTimer tm(p, EV_INTERP);
+    if (p->prec == NUFFT_F64)
+        CK(launch_interp<double>(p->geom, pts_view<double>(p), p->nbins,
+                                 static_cast<const double2*>(grid_dev),
+                                 static_cast<double2*>(c_dev), p->beta, p->stream));
+    else
+        CK(launch_interp<float>(p->geom, pts_view<float>(p), p->nbins,
+                                static_cast<const float2*>(grid_dev), static_cast<float2*>(c_dev),
+                                p->beta, p->stream));
+    return NUFFT_OK;
+}
+
+int do_fft(nufft_plan_s* p, int sign) {
+    StageTimer tm(p, EV_FFT);
+    const int dir = sign < 0 ? CUFFT_FORWARD : CUFFT_INVERSE;
+    cufftResult r;
+    if (p->prec == NUFFT_F64)
+        r = cufftExecZ2Z(p->fft, static_cast<cufftDoubleComplex*>(p->d_grid),
+                         static_cast<cufftDoubleComplex*>(p->d_grid), dir);
+    else
+        r = cufftExecC2C(p->fft, static_cast<cufftComplex*>(p->d_grid),
+                         static_cast<cufftComplex*>(p->d_grid), dir);
+    return r == CUFFT_SUCCESS ? NUFFT_OK : NUFFT_ERR_CUFFT;
+}
+
+}  // namespace
+
+extern "C" {
+
+int nufft_default_opts(nufft_opts* o) {
+    if (!o) return NUFFT_ERR_ARG;
+    std::memset(o, 0, sizeof(*o));
+    o->L = 2.0 * M_PI;
+    return NUFFT_OK;
+}
+
+const char* nufft_strerror(int code) {
+    switch (code) {
+        case NUFFT_OK: return "ok";
+        case NUFFT_WARN_EPS_CLAMPED: return "warning: eps clamped to the supported range";
+        case NUFFT_ERR_ARG: return "invalid argument";
+        case NUFFT_ERR_MODES: return "invalid mode counts (need even N >= 2 with 2N >= w)";
+        case NUFFT_ERR_NPTS: return "invalid number of points";
+        case NUFFT_ERR_NOT_SET: return "points not set (call nufft_setpts first)";
+        case NUFFT_ERR_ALLOC: return "device allocation failed";
+        case NUFFT_ERR_CUDA: return "CUDA error";
+        case NUFFT_ERR_CUFFT: return "cuFFT error";
+        case NUFFT_ERR_NCCL: return "NCCL error";
+        case NUFFT_ERR_UNSUPPORTED: return "unsupported option";
+        default: return "unknown status";
+    }
+}
+
+int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int precision,
+               const nufft_opts* opts, nufft_handle* out) {
+    if (!out) return NUFFT_ERR_ARG;
+    *out = nullptr;
+    if (precision != NUFFT_F32 && precision != NUFFT_F64) return NUFFT_ERR_ARG;
+    nufft_opts o;
+    if (opts) o = *opts;
+    else nufft_default_opts(&o);
+    if (!(o.L > 0) || (o.modeord != 0 && o.modeord != 1)) return NUFFT_ERR_ARG;
+    if (o.comm) return NUFFT_ERR_UNSUPPORTED;
+
+    nufft_plan_s* p = new (std::nothrow) nufft_plan_s();
+    if (!p) return NUFFT_ERR_ALLOC;
+    int status = select_width(eps, precision, &p->w, &p->beta, &p->eps);
+    const int64_t Nv[3] = {N1, N2, N3};
+    for (int d = 0; d < 3; ++d) {
+        if (Nv[d] < 2 || (Nv[d] & 1) || 2 * Nv[d] < p->w) {
+            delete p;
+            return NUFFT_ERR_MODES;
+        }
+        p->N[d] = Nv[d];
+        p->nf[d] = 2 * Nv[d];  // sigma = 2 (reading R8)
+    }
+    p->prec = precision;
+    p->iflag = iflag >= 0 ? 1 : -1;
+    p->modeord = o.modeord;
+    p->stream = static_cast<cudaStream_t>(o.stream);
+    p->real_size = precision == NUFFT_F64 ? 8 : 4;
+    p->cplx_size = 2 * p->real_size;
+    p->timing = o.timing != 0;
+
+    Geom& g = p->geom;
+    for (int d = 0; d < 3; ++d) {
+        g.nf[d] = p->nf[d];
+        int t = o.tile[d] > 0 ? o.tile[d] : default_tile(p->w, precision, p->nf[d]);
+        if (t > 255 || t > p->nf[d]) {
+            delete p;
+            return NUFFT_ERR_ARG;
+        }
+        g.T[d] = t;
+        g.nb[d] = (int)((p->nf[d] + t - 1) / t);
+        g.scale[d] = (double)p->nf[d] / o.L;
+    }
+    g.L = o.L;
+    g.w = p->w;
+    g.z_lo = 0;
+    g.nz_loc = p->nf[2];
+    p->nbins = (int64_t)g.nb[0] * g.nb[1] * g.nb[2];
+
+    int st = NUFFT_OK;
+    // deconvolution factors p_d(n) = 2 / (w phihat(pi n w / nf_d)) (R6)
+    for (int d = 0; d < 3 && !st; ++d) {
+        std::vector<double> pd((size_t)p->N[d]);
+        for (int64_t i = 0; i < p->N[d]; ++i) {
+            const double n = (double)(i - p->N[d] / 2);
+            pd[(size_t)i] = 2.0 / ((double)p->w *
+                                   es_phihat(M_PI * n * (double)p->w / (double)p->nf[d], p->beta));
+        }
+        st = dev_alloc(p, &p->d_p[d], (size_t)p->N[d] * p->real_size);
+        if (st) break;
+        if (precision == NUFFT_F64) {
+            st = cuda_status(cudaMemcpy(p->d_p[d], pd.data(), pd.size() * 8, cudaMemcpyHostToDevice));
+        } else {
+            std::vector<float> pf(pd.begin(), pd.end());
+            st = cuda_status(cudaMemcpy(p->d_p[d], pf.data(), pf.size() * 4, cudaMemcpyHostToDevice));
+        }
+    }
+    p->grid_bytes = (size_t)(p->nf[0] * p->nf[1] * p->nf[2]) * p->cplx_size;
+    if (!st) st = dev_alloc(p, &p->d_grid, p->grid_bytes);
+    if (!st) st = dev_alloc(p, (void**)&p->count, sizeof(uint32_t) * (size_t)p->nbins);
+    if (!st) st = dev_alloc(p, (void**)&p->offset, sizeof(uint32_t) * (size_t)(p->nbins + 1));
+    if (!st) st = dev_alloc(p, (void**)&p->blocksum, sizeof(uint32_t) * scan_blocksum_elems(p->nbins));
+    if (!st) {
+        cufftResult r = cufftPlan3d(&p->fft, (int)p->nf[2], (int)p->nf[1], (int)p->nf[0],
+                                    precision == NUFFT_F64 ? CUFFT_Z2Z : CUFFT_C2C);
+        if (r != CUFFT_SUCCESS) st = NUFFT_ERR_CUFFT;
+        else {
+            p->fft_ok = true;
+            size_t ws = 0;
+            cufftGetSize(p->fft, &ws);
+            p->bytes += ws;
+            if (cufftSetStream(p->fft, p->stream) != CUFFT_SUCCESS) st = NUFFT_ERR_CUFFT;
+        }
+    }
+    if (!st && p->timing)
+        for (int i = 0; i < 8; ++i) {
+            cudaEventCreate(&p->ev0[i]);
+            cudaEventCreate(&p->ev[i]);
+        }
+    if (st) {
+        nufft_destroy(p);
+        return st;
+    }
+    *out = p;
+    return status;
+}
+
+int nufft_setpts(nufft_handle p, int64_t Np, const void* x, const void* y, const void* z) {
+    if (!p) return NUFFT_ERR_ARG;
+    if (Np < 0 || Np >= (int64_t)1 << 31) return NUFFT_ERR_NPTS;
+    if (Np > 0 && (!x || !y || !z)) return NUFFT_ERR_ARG;
+    StageTimer tm(p, EV_SETPTS);
+    int st = NUFFT_OK;
+    if (Np > p->cap) {
+        dev_free(p, (void**)&p->bin_of, 4 * p->cap);
+        dev_free(p, (void**)&p->rank_of, 4 * p->cap);
+        dev_free(p, (void**)&p->perm, 4 * p->cap);
+        dev_free(p, (void**)&p->la, 4 * p->cap);
+        dev_free(p, &p->dx, p->real_size * p->cap);
+        dev_free(p, &p->dy, p->real_size * p->cap);
+        dev_free(p, &p->dz, p->real_size * p->cap);
+        p->cap = 0;
+        const size_t n = (size_t)Np;
+        st = dev_alloc(p, (void**)&p->bin_of, 4 * n);
+        if (!st) st = dev_alloc(p, (void**)&p->rank_of, 4 * n);
+        if (!st) st = dev_alloc(p, (void**)&p->perm, 4 * n);
+        if (!st) st = dev_alloc(p, (void**)&p->la, 4 * n);
+        if (!st) st = dev_alloc(p, &p->dx, p->real_size * n);
+        if (!st) st = dev_alloc(p, &p->dy, p->real_size * n);
+        if (!st) st = dev_alloc(p, &p->dz, p->real_size * n);
+        if (st) {
+            p->Np = -1;
+            return st;
+        }
+        p->cap = Np;
+    }
+    const size_t b = (size_t)Np * p->real_size;
+    const void *xd = nullptr, *yd = nullptr, *zd = nullptr;
+    if ((st = input_view(p, x, b, 0, 3 * b, &xd))) return st;
+    if ((st = input_view(p, y, b, b, 3 * b, &yd))) return st;
+    if ((st = input_view(p, z, b, 2 * b, 3 * b, &zd))) return st;
+    if (p->prec == NUFFT_F64)
+        CK(launch_bin_sort<double>(p->geom, Np, static_cast<const double*>(xd),
+                                   static_cast<const double*>(yd), static_cast<const double*>(zd),
+                                   p->count, p->offset, p->blocksum, p->bin_of, p->rank_of,
+                                   p->perm, static_cast<double*>(p->dx),
+                                   static_cast<double*>(p->dy), static_cast<double*>(p->dz),
+                                   p->la, p->nbins, p->stream));
+    else
+        CK(launch_bin_sort<float>(p->geom, Np, static_cast<const float*>(xd),
+                                  static_cast<const float*>(yd), static_cast<const float*>(zd),
+                                  p->count, p->offset, p->blocksum, p->bin_of, p->rank_of,
+                                  p->perm, static_cast<float*>(p->dx), static_cast<float*>(p->dy),
+                                  static_cast<float*>(p->dz), p->la, p->nbins, p->stream));
+    p->Np = Np;
+    return NUFFT_OK;
+}
+
+int nufft_execute_type1(nufft_handle p, const void* c, void* fk) {
+    if (!p || !fk || (!c && p->Np > 0)) return NUFFT_ERR_ARG;
+    if (p->Np < 0) return NUFFT_ERR_NOT_SET;
+    int st;
+    const void* cd = nullptr;
+    if ((st = input_view(p, c, (size_t)p->Np * p->cplx_size, 0, (size_t)p->Np * p->cplx_size, &cd)))
+        return st;
+    const size_t fk_bytes = (size_t)(p->N[0] * p->N[1] * p->N[2]) * p->cplx_size;
+    void* fkd = nullptr;
+    bool staged = false;
+    if ((st = output_view(p, fk, fk_bytes, &fkd, &staged))) return st;
+    if ((st = do_spread(p, cd, p->d_grid))) return st;                 // Step 1: C
+    if ((st = do_fft(p, p->iflag))) return st;                          // Step 2: F
+    {
+        StageTimer tm(p, EV_DECONV);                                    // Steps 3, 4: chi, D
+        if (p->prec == NUFFT_F64)
+            CK(launch_truncate_deconv<double>(
+                static_cast<const double2*>(p->d_grid), p->nf, p->N,
+                static_cast<const double*>(p->d_p[0]), static_cast<const double*>(p->d_p[1]),
+                static_cast<const double*>(p->d_p[2]), p->modeord, static_cast<double2*>(fkd),
+                p->stream));
+        else
+            CK(launch_truncate_deconv<float>(
+                static_cast<const float2*>(p->d_grid), p->nf, p->N,
+                static_cast<const float*>(p->d_p[0]), static_cast<const float*>(p->d_p[1]),
+                static_cast<const float*>(p->d_p[2]), p->modeord, static_cast<float2*>(fkd),
+                p->stream));
+    }
+    return finish_output(p, fk, fkd, fk_bytes, staged);
+}
+
+int nufft_execute_type2(nufft_handle p, const void* fk, void* c) {
+    if (!p || !fk || (!c && p->Np > 0)) return NUFFT_ERR_ARG;
+    if (p->Np < 0) return NUFFT_ERR_NOT_SET;
+    int st;
+    const size_t fk_bytes = (size_t)(p->N[0] * p->N[1] * p->N[2]) * p->cplx_size;
+    const void* fkd = nullptr;
+    if ((st = input_view(p, fk, fk_bytes, 0, fk_bytes, &fkd))) return st;
+    const size_t c_bytes = (size_t)p->Np * p->cplx_size;
+    void* cd = nullptr;
+    bool staged = false;
+    if ((st = output_view(p, c, c_bytes, &cd, &staged))) return st;
+    {
+        StageTimer tm(p, EV_PAD);                                       // D, chi^T
+        if (p->prec == NUFFT_F64)
+            CK(launch_pad_precorrect<double>(
+                static_cast<const double2*>(fkd), p->N, static_cast<const double*>(p->d_p[0]),
+                static_cast<const double*>(p->d_p[1]), static_cast<const double*>(p->d_p[2]),
+                p->modeord, p->nf, static_cast<double2*>(p->d_grid), p->stream));
+        else
+            CK(launch_pad_precorrect<float>(
+                static_cast<const float2*>(fkd), p->N, static_cast<const float*>(p->d_p[0]),
+                static_cast<const float*>(p->d_p[1]), static_cast<const float*>(p->d_p[2]),
+                p->modeord, p->nf, static_cast<float2*>(p->d_grid), p->stream));
+    }
+    if ((st = do_fft(p, -p->iflag))) return st;                         // F^-1
+    if ((st = do_interp(p, p->d_grid, cd))) return st;                  // C^T
+    return finish_output(p, c, cd, c_bytes, staged);
+}
+
+int nufft_spread(nufft_handle p, const void* c, void* grid) {
+    if (!p || !grid || (!c && p->Np > 0)) return NUFFT_ERR_ARG;
+    if (p->Np < 0) return NUFFT_ERR_NOT_SET;
+    int st;
+    const void* cd = nullptr;
+    if ((st = input_view(p, c, (size_t)p->Np * p->cplx_size, 0, (size_t)p->Np * p->cplx_size, &cd)))
+        return st;
+    void* gd = nullptr;
+    bool staged = false;
+    if ((st = output_view(p, grid, p->grid_bytes, &gd, &staged))) return st;
+    if ((st = do_spread(p, cd, gd))) return st;
+    return finish_output(p, grid, gd, p->grid_bytes, staged);
+}
+
+int nufft_interp(nufft_handle p, const void* grid, void* c) {
+    if (!p || !grid || (!c && p->Np > 0)) return NUFFT_ERR_ARG;
+    if (p->Np < 0) return NUFFT_ERR_NOT_SET;
+    int st;
+    const void* gd = nullptr;
+    if ((st = input_view(p, grid, p->grid_bytes, 0, p->grid_bytes, &gd))) return st;
+    const size_t c_bytes = (size_t)p->Np * p->cplx_size;
+    void* cd = nullptr;
+    bool staged = false;
+    if ((st = output_view(p, c, c_bytes, &cd, &staged))) return st;
+    if ((st = do_interp(p, gd, cd))) return st;
+    return finish_output(p, c, cd, c_bytes, staged);
+}
+
+int nufft_destroy(nufft_handle p) {
+    if (!p) return NUFFT_OK;
+    if (p->stream) cudaStreamSynchronize(p->stream);
+    else cudaDeviceSynchronize();
+    if (p->fft_ok) cufftDestroy(p->fft);
+    for (int d = 0; d < 3; ++d) dev_free(p, &p->d_p[d], 0);
+    dev_free(p, &p->d_grid, 0);
+    dev_free(p, (void**)&p->count, 0);
+    dev_free(p, (void**)&p->offset, 0);
+    dev_free(p, (void**)&p->blocksum, 0);
+    dev_free(p, (void**)&p->bin_of, 0);
+    dev_free(p, (void**)&p->rank_of, 0);
+    dev_free(p, (void**)&p->perm, 0);
+    dev_free(p, (void**)&p->la, 0);
+    dev_free(p, &p->dx, 0);
+    dev_free(p, &p->dy, 0);
+    dev_free(p, &p->dz, 0);
+    dev_free(p, &p->stage_in, 0);
+    dev_free(p, &p->stage_out, 0);
+    if (p->timing)
+        for (int i = 0; i < 8; ++i) {
+            if (p->ev0[i]) cudaEventDestroy(p->ev0[i]);
+            if (p->ev[i]) cudaEventDestroy(p->ev[i]);
+        }
+    delete p;
+    return NUFFT_OK;
+}
+
+int nufft_get_info(nufft_handle p, nufft_info* info) {
+    if (!p || !info) return NUFFT_ERR_ARG;
+    std::memset(info, 0, sizeof(*info));
+    info->precision = p->prec;
+    info->w = p->w;
+    info->beta = p->beta;
+    info->eps = p->eps;
+    for (int d = 0; d < 3; ++d) {
+        info->N[d] = p->N[d];
+        info->nf[d] = p->nf[d];
+        info->tile[d] = p->geom.T[d];
+    }
+    info->nbins = p->nbins;
+    info->Np = p->Np;
+    info->device_bytes = p->bytes;
+    info->nranks = 1;
+    info->rank = 0;
+    info->slab_lo = 0;
+    info->slab_hi = p->nf[2];
+    float ms[8];
+    for (int i = 0; i < 8; ++i) {
+        ms[i] = -1.0f;
+        if (p->timing && p->ev_used[i] && cudaEventSynchronize(p->ev[i]) == cudaSuccess)
+            cudaEventElapsedTime(&ms[i], p->ev0[i], p->ev[i]);
+    }
+    info->ms_setpts = ms[EV_SETPTS];
+    info->ms_spread = ms[EV_SPREAD];
+    info->ms_fold = -1;
+    info->ms_fft = ms[EV_FFT];
+    info->ms_deconv = ms[EV_DECONV];
+    info->ms_pad = ms[EV_PAD];
+    info->ms_interp = ms[EV_INTERP];
+    info->ms_comm = -1;
+    return NUFFT_OK;
+}
+
+int nufft_comm_unique_id(char id[128]) {
+    (void)id;
+    return NUFFT_ERR_UNSUPPORTED;
+}
+int nufft_comm_init(const char id[128], int nranks, int rank, void** comm) {
+    (void)id, (void)nranks, (void)rank, (void)comm;
+    return NUFFT_ERR_UNSUPPORTED;
+}
+int nufft_comm_destroy(void* comm) {
+    (void)comm;
+    return NUFFT_ERR_UNSUPPORTED;
+}
+int nufft_local_modes(nufft_handle p, int64_t lo[3], int64_t hi[3]) {
+    if (!p || !lo || !hi) return NUFFT_ERR_ARG;
+    for (int d = 0; d < 3; ++d) {
+        lo[d] = 0;
+        hi[d] = p->N[d];
+    }
+    return NUFFT_OK;
+}
+
+}  // extern "C"

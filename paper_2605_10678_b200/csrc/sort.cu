@@ -1,0 +1,242 @@
+// sort.cu -- setpts: fold + bin count, exclusive scan, scatter (counting sort).
+//
+// PAPER.md:204 ("sort particles into spatial tiles of tunable size") and
+// PAPER.md:226-227 (bin sorting for interpolation locality).  north_star (1):
+// "a bin-sort of points by subgrid cell, using a counting sort built from
+// warp-level prefix scans".
+//
+//   k1 bin_count : per point, fold onto the torus and rescale in fp64
+//                  (s = x * nf / L), bin = tile of floor(s); a warp-aggregated
+//                  atomicAdd on count[bin] (lanes of one bin share one atomic via
+//                  __match_any_sync) returns each point's rank inside its bin.
+//   k2 scan      : exclusive prefix sum of count[] -> offset[] with warp
+//                  __shfl_up_sync scans, three phases (tile sums, scan of sums,
+//                  tile scans + carry-in).
+//   k3 scatter   : slot = offset[bin] + rank; perm[slot] = j and the sorted
+//                  stencil record (local base la, phase offsets d) for the slot.
+#include "internal.cuh"
+
+namespace nufft {
+
+namespace {
+
+constexpr int kSortThreads = 256;
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 4;                        // per thread
+constexpr int kScanTile = kScanThreads * kScanItems;  // counts per scan tile
+
+// Fold onto [0, L) and rescale to fine-grid units (reading R10), fp64.
+__device__ __forceinline__ double fold_rescale(double x, double L, double scale, int64_t nf) {
+    double xf = x - L * floor(x / L);
+    double s = xf * scale;
+    if (s >= (double)nf) s -= (double)nf;
+    if (s < 0.0) s += (double)nf;
+    return s;
+}
+
+__device__ __forceinline__ int cell_of(double s, int64_t nf) {
+    int64_t c = (int64_t)s;  // s >= 0: truncation == floor
+    return (int)(c >= nf ? nf - 1 : c);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kSortThreads) bin_count_kernel(
+    Geom g, int64_t Np, const T* __restrict__ x, const T* __restrict__ y,
+    const T* __restrict__ z, uint32_t* __restrict__ count, uint32_t* __restrict__ bin_of,
+    uint32_t* __restrict__ rank_of) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i - lane < Np;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const bool live = i < Np;
+        uint32_t bin = 0xffffffffu;
+        if (live) {
+            int cx = cell_of(fold_rescale((double)x[i], g.L, g.scale[0], g.nf[0]), g.nf[0]);
+            int cy = cell_of(fold_rescale((double)y[i], g.L, g.scale[1], g.nf[1]), g.nf[1]);
+            int cz = cell_of(fold_rescale((double)z[i], g.L, g.scale[2], g.nf[2]), g.nf[2]) -
+                     (int)g.z_lo;
+            bin = (uint32_t)(cx / g.T[0]) +
+                  (uint32_t)g.nb[0] * ((uint32_t)(cy / g.T[1]) + (uint32_t)g.nb[1] * (uint32_t)(cz / g.T[2]));
+        }
+        // warp-aggregated atomic: one atomicAdd per distinct bin in the warp
+        const unsigned active = __ballot_sync(0xffffffffu, live);
+        if (live) {
+            const unsigned peers = __match_any_sync(active, bin);
+            const int leader = __ffs(peers) - 1;
+            const unsigned below = peers & ((1u << lane) - 1u);
+            uint32_t base = 0;
+            if (lane == leader) base = atomicAdd(&count[bin], (uint32_t)__popc(peers));
+            base = __shfl_sync(peers, base, leader);
+            bin_of[i] = bin;
+            rank_of[i] = base + (uint32_t)__popc(below);
+        }
+    }
+}
+
+// Inclusive warp scan with __shfl_up_sync.
+__device__ __forceinline__ uint32_t warp_inclusive_scan(uint32_t v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    return v;
+}
+
+// Block-wide exclusive scan of one value per thread; returns the exclusive
+// prefix and writes the block total to *total.
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* total) {
+    __shared__ uint32_t warp_sums[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nwarps = blockDim.x >> 5;
+    uint32_t inc = warp_inclusive_scan(v);
+    if (lane == 31) warp_sums[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t s = lane < nwarps ? warp_sums[lane] : 0u;
+        uint32_t si = warp_inclusive_scan(s);
+        if (lane < nwarps) warp_sums[lane] = si - s;  // exclusive warp offsets
+        if (lane == nwarps - 1) *total = si;
+    }
+    __syncthreads();
+    uint32_t r = inc - v + warp_sums[warp];
+    __syncthreads();
+    return r;
+}
+
+// phase 1: per scan tile, the sum of its counts
+__global__ void __launch_bounds__(kScanThreads) scan_tile_sums(const uint32_t* __restrict__ count,
+                                                               int64_t n,
+                                                               uint32_t* __restrict__ sums) {
+    const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    uint32_t v = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k)
+        if (base + k < n) v += count[base + k];
+    // warp reduce, then block reduce via the scan helper's total
+    __shared__ uint32_t total;
+    (void)block_exclusive_scan(v, &total);
+    if (threadIdx.x == 0) sums[blockIdx.x] = total;
+}
+
+// phase 2: one block scans the tile sums in place (exclusive), any length
+__global__ void __launch_bounds__(kScanThreads) scan_sums(uint32_t* __restrict__ sums,
+                                                          int64_t nsums) {
+    __shared__ uint32_t total;
+    uint32_t carry = 0;
+    for (int64_t base = 0; base < nsums; base += blockDim.x) {
+        int64_t i = base + threadIdx.x;
+        uint32_t v = i < nsums ? sums[i] : 0u;
+        uint32_t ex = block_exclusive_scan(v, &total);
+        if (i < nsums) sums[i] = ex + carry;
+        carry += total;
+        __syncthreads();
+    }
+}
+
+// phase 3: each tile re-scans its counts and adds its carry-in; offset[n] = total
+__global__ void __launch_bounds__(kScanThreads) scan_tiles(const uint32_t* __restrict__ count,
+                                                           int64_t n,
+                                                           const uint32_t* __restrict__ sums,
+                                                           uint32_t* __restrict__ offset) {
+    const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    uint32_t v[kScanItems];
+    uint32_t tsum = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        v[k] = base + k < n ? count[base + k] : 0u;
+        tsum += v[k];
+    }
+    __shared__ uint32_t total;
+    uint32_t ex = block_exclusive_scan(tsum, &total) + sums[blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        if (base + k < n) offset[base + k] = ex;
+        ex += v[k];
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == blockDim.x - 1) offset[n] = ex;
+}
+
+// Bin-local stencil record of one coordinate (reading R4: a = ceil(s - w/2)).
+//   r  = s - (bin origin)          exact in fp64
+//   ls = r + floor(w/2)            coordinate relative to the tile origin
+//   la = ceil(ls - w/2)            local stencil base, in [0, T]
+//   d  = ls - la                   phase offset, z_k = 2 (k - d) / w
+__device__ __forceinline__ void local_stencil(double s, int c, int T, int w, int* la, double* d) {
+    const int origin = (c / T) * T;
+    const double ls = (s - (double)origin) + (double)(w / 2);
+    const double a = ceil(ls - 0.5 * (double)w);
+    *la = (int)a;
+    *d = ls - a;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kSortThreads) scatter_kernel(
+    Geom g, int64_t Np, const T* __restrict__ x, const T* __restrict__ y,
+    const T* __restrict__ z, const uint32_t* __restrict__ bin_of,
+    const uint32_t* __restrict__ rank_of, const uint32_t* __restrict__ offset,
+    uint32_t* __restrict__ perm, T* __restrict__ dx, T* __restrict__ dy, T* __restrict__ dz,
+    uint32_t* __restrict__ la) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < Np;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t slot = offset[bin_of[i]] + rank_of[i];
+        const double sx = fold_rescale((double)x[i], g.L, g.scale[0], g.nf[0]);
+        const double sy = fold_rescale((double)y[i], g.L, g.scale[1], g.nf[1]);
+        const double sz = fold_rescale((double)z[i], g.L, g.scale[2], g.nf[2]) - (double)g.z_lo;
+        int lax, lay, laz;
+        double ddx, ddy, ddz;
+        local_stencil(sx, cell_of(sx, g.nf[0]), g.T[0], g.w, &lax, &ddx);
+        local_stencil(sy, cell_of(sy, g.nf[1]), g.T[1], g.w, &lay, &ddy);
+        local_stencil(sz, cell_of(sz + (double)g.z_lo, g.nf[2]) - (int)g.z_lo, g.T[2], g.w, &laz,
+                      &ddz);
+        perm[slot] = (uint32_t)i;
+        dx[slot] = (T)ddx;
+        dy[slot] = (T)ddy;
+        dz[slot] = (T)ddz;
+        la[slot] = (uint32_t)lax | ((uint32_t)lay << 8) | ((uint32_t)laz << 16);
+    }
+}
+
+inline int grid_for(int64_t n, int threads) {
+    int64_t b = (n + threads - 1) / threads;
+    const int64_t cap = 148 * 16;  // persistent-style cap: 16 resident CTAs per SM
+    if (b > cap) b = cap;
+    return (int)(b < 1 ? 1 : b);
+}
+
+}  // namespace
+
+size_t scan_blocksum_elems(int64_t nbins) { return (size_t)((nbins + kScanTile - 1) / kScanTile) + 1; }
+
+template <typename T>
+cudaError_t launch_bin_sort(const Geom& g, int64_t Np, const T* x, const T* y, const T* z,
+                            uint32_t* count, uint32_t* offset, uint32_t* blocksum,
+                            uint32_t* bin_of, uint32_t* rank_of, uint32_t* perm, T* dx, T* dy,
+                            T* dz, uint32_t* la, int64_t nbins, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(count, 0, sizeof(uint32_t) * (size_t)nbins, s);
+    if (e != cudaSuccess) return e;
+    if (Np > 0) {
+        bin_count_kernel<T><<<grid_for(Np, kSortThreads), kSortThreads, 0, s>>>(
+            g, Np, x, y, z, count, bin_of, rank_of);
+    }
+    const int64_t ntiles = (nbins + kScanTile - 1) / kScanTile;
+    scan_tile_sums<<<(unsigned)ntiles, kScanThreads, 0, s>>>(count, nbins, blocksum);
+    scan_sums<<<1, kScanThreads, 0, s>>>(blocksum, ntiles);
+    scan_tiles<<<(unsigned)ntiles, kScanThreads, 0, s>>>(count, nbins, blocksum, offset);
+    if (Np > 0) {
+        scatter_kernel<T><<<grid_for(Np, kSortThreads), kSortThreads, 0, s>>>(
+            g, Np, x, y, z, bin_of, rank_of, offset, perm, dx, dy, dz, la);
+    }
+    return cudaGetLastError();
+}
+
+template cudaError_t launch_bin_sort<float>(const Geom&, int64_t, const float*, const float*,
+                                            const float*, uint32_t*, uint32_t*, uint32_t*,
+                                            uint32_t*, uint32_t*, uint32_t*, float*, float*,
+                                            float*, uint32_t*, int64_t, cudaStream_t);
+template cudaError_t launch_bin_sort<double>(const Geom&, int64_t, const double*, const double*,
+                                             const double*, uint32_t*, uint32_t*, uint32_t*,
+                                             uint32_t*, uint32_t*, uint32_t*, double*, double*,
+                                             double*, uint32_t*, int64_t, cudaStream_t);
+
+}  // namespace nufft

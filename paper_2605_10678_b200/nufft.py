@@ -1,0 +1,225 @@
+"""Thin ctypes binding of libnufft.so (include/nufft.h) -- argument marshalling only.
+
+Every step of the NUFFT runs in the library's CUDA kernels (and cuFFT).  This
+module converts torch tensors to raw pointers, passes the current CUDA stream
+and raises on non-zero status.  There is NO CPU fallback: if the shared library
+is missing or CUDA is absent the calls fail loudly.
+
+    import torch, paper_2605_10678_b200 as nb
+    plan = nb.Plan((N1, N2, N3), eps=1e-6, precision="f64")   # iflag=-1: Eq. (1)
+    plan.setpts(x, y, z)          # torch tensors, CUDA (or pinned host) memory
+    fk = plan.type1(c)            # (N3, N2, N1) complex, centered modes
+    c2 = plan.type2(fk)           # (Np,) complex, caller order
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libnufft.so")
+
+F32, F64 = 0, 1
+
+
+class NufftError(RuntimeError):
+    pass
+
+
+class Opts(ctypes.Structure):
+    _fields_ = [("L", ctypes.c_double), ("modeord", ctypes.c_int), ("stream", ctypes.c_void_p),
+                ("comm", ctypes.c_void_p), ("points_owned", ctypes.c_int),
+                ("tile", ctypes.c_int * 3), ("timing", ctypes.c_int),
+                ("reserved", ctypes.c_int * 7)]
+
+
+class Info(ctypes.Structure):
+    _fields_ = [("precision", ctypes.c_int), ("w", ctypes.c_int), ("beta", ctypes.c_double),
+                ("eps", ctypes.c_double), ("N", ctypes.c_int64 * 3), ("nf", ctypes.c_int64 * 3),
+                ("tile", ctypes.c_int * 3), ("nbins", ctypes.c_int64), ("Np", ctypes.c_int64),
+                ("device_bytes", ctypes.c_size_t), ("nranks", ctypes.c_int),
+                ("rank", ctypes.c_int), ("slab_lo", ctypes.c_int64), ("slab_hi", ctypes.c_int64),
+                ("ms_setpts", ctypes.c_float), ("ms_spread", ctypes.c_float),
+                ("ms_fold", ctypes.c_float), ("ms_fft", ctypes.c_float),
+                ("ms_deconv", ctypes.c_float), ("ms_pad", ctypes.c_float),
+                ("ms_interp", ctypes.c_float), ("ms_comm", ctypes.c_float)]
+
+    def as_dict(self):
+        d = {}
+        for name, _ in self._fields_:
+            v = getattr(self, name)
+            d[name] = list(v) if hasattr(v, "__len__") else v
+        return d
+
+
+_EXPORTS = ["nufft_default_opts", "nufft_plan", "nufft_setpts", "nufft_execute_type1",
+            "nufft_execute_type2", "nufft_spread", "nufft_interp", "nufft_destroy",
+            "nufft_get_info", "nufft_strerror", "nufft_comm_unique_id", "nufft_comm_init",
+            "nufft_comm_destroy", "nufft_local_modes"]
+
+_lib = None
+
+
+def lib():
+    """Load libnufft.so (raises if it was not built: no fallback path exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise NufftError(f"{LIB_PATH} missing: run `python -m paper_2605_10678_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        vp = ctypes.c_void_p
+        L.nufft_default_opts.argtypes = [ctypes.POINTER(Opts)]
+        L.nufft_plan.argtypes = [ctypes.c_int64] * 3 + [ctypes.c_int, ctypes.c_double, ctypes.c_int,
+                                                        ctypes.POINTER(Opts), ctypes.POINTER(vp)]
+        L.nufft_setpts.argtypes = [vp, ctypes.c_int64, vp, vp, vp]
+        for f in ("nufft_execute_type1", "nufft_execute_type2", "nufft_spread", "nufft_interp"):
+            getattr(L, f).argtypes = [vp, vp, vp]
+        L.nufft_destroy.argtypes = [vp]
+        L.nufft_get_info.argtypes = [vp, ctypes.POINTER(Info)]
+        L.nufft_strerror.argtypes = [ctypes.c_int]
+        L.nufft_strerror.restype = ctypes.c_char_p
+        L.nufft_comm_unique_id.argtypes = [ctypes.c_char_p]
+        L.nufft_comm_init.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_int,
+                                      ctypes.POINTER(vp)]
+        L.nufft_comm_destroy.argtypes = [vp]
+        L.nufft_local_modes.argtypes = [vp, ctypes.POINTER(ctypes.c_int64),
+                                        ctypes.POINTER(ctypes.c_int64)]
+        _lib = L
+    return _lib
+
+
+def _check(st: int, what: str) -> int:
+    if st >= 2:
+        raise NufftError(f"{what}: {lib().nufft_strerror(st).decode()} (status {st})")
+    return st
+
+
+def _ptr(t: torch.Tensor, dtype, n: int, name: str) -> int:
+    if t.dtype != dtype:
+        raise TypeError(f"{name}: expected {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if t.numel() != n:
+        raise ValueError(f"{name}: expected {n} elements, got {t.numel()}")
+    return t.data_ptr()
+
+
+class Plan:
+    """One NUFFT plan (type 1 and type 2 share the points and the fine grid).
+
+    N        : (N1, N2, N3) even mode counts
+    eps      : tolerance (relative l2), selects the ES width w (R1)
+    precision: "f32" | "f64"
+    iflag    : sign of the type-1 exponent (-1 = PAPER.md Eq. 1); type 2 uses -iflag
+    L        : period of the point domain [0, L)^3
+    """
+
+    def __init__(self, N, eps, precision="f64", iflag=-1, L=2 * math.pi, modeord=0,
+                 device=None, stream=None, tile=None, timing=False):
+        if not torch.cuda.is_available():
+            raise NufftError("libnufft requires a CUDA device (no CPU fallback)")
+        self.N = tuple(int(n) for n in N)
+        self.precision = precision
+        self.prec = F64 if precision in ("f64", "double", torch.float64) else F32
+        self.real = torch.float64 if self.prec == F64 else torch.float32
+        self.cplx = torch.complex128 if self.prec == F64 else torch.complex64
+        self.device = torch.device(device) if device is not None else torch.device("cuda",
+                                                                                   torch.cuda.current_device())
+        self._stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        o = Opts()
+        lib().nufft_default_opts(ctypes.byref(o))
+        o.L = float(L)
+        o.modeord = int(modeord)
+        o.stream = self._stream.cuda_stream
+        o.timing = 1 if timing else 0
+        if tile is not None:
+            for d in range(3):
+                o.tile[d] = int(tile[d] if hasattr(tile, "__len__") else tile)
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            st = lib().nufft_plan(self.N[0], self.N[1], self.N[2], int(iflag), float(eps), self.prec,
+                                  ctypes.byref(o), ctypes.byref(h))
+        _check(st, "nufft_plan")
+        self.status = st
+        self._h = h
+        self.Np = None
+
+    # -- lifecycle
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().nufft_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- calls
+    def info(self) -> dict:
+        i = Info()
+        _check(lib().nufft_get_info(self._h, ctypes.byref(i)), "nufft_get_info")
+        return i.as_dict()
+
+    def setpts(self, x: torch.Tensor, y: torch.Tensor, z: torch.Tensor):
+        n = x.numel()
+        px = _ptr(x, self.real, n, "x")
+        py = _ptr(y, self.real, n, "y")
+        pz = _ptr(z, self.real, n, "z")
+        with torch.cuda.device(self.device):
+            _check(lib().nufft_setpts(self._h, n, px, py, pz), "nufft_setpts")
+        self.Np = n
+        return self
+
+    def _out(self, out, shape, on_host_like=None):
+        if out is not None:
+            return out
+        dev = self.device if on_host_like is None or on_host_like.is_cuda else torch.device("cpu")
+        return torch.empty(shape, dtype=self.cplx, device=dev,
+                           pin_memory=(dev.type == "cpu" and torch.cuda.is_available()))
+
+    def type1(self, c: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        N1, N2, N3 = self.N
+        fk = self._out(out, (N3, N2, N1), c)
+        pc = _ptr(c, self.cplx, self.Np, "c")
+        pf = _ptr(fk, self.cplx, N1 * N2 * N3, "fk")
+        with torch.cuda.device(self.device):
+            _check(lib().nufft_execute_type1(self._h, pc, pf), "nufft_execute_type1")
+        return fk
+
+    def type2(self, fk: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        N1, N2, N3 = self.N
+        c = self._out(out, (self.Np,), fk)
+        pf = _ptr(fk, self.cplx, N1 * N2 * N3, "fk")
+        pc = _ptr(c, self.cplx, self.Np, "c")
+        with torch.cuda.device(self.device):
+            _check(lib().nufft_execute_type2(self._h, pf, pc), "nufft_execute_type2")
+        return c
+
+    def spread(self, c: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        N1, N2, N3 = self.N
+        g = self._out(out, (2 * N3, 2 * N2, 2 * N1), c)
+        pc = _ptr(c, self.cplx, self.Np, "c")
+        pg = _ptr(g, self.cplx, 8 * N1 * N2 * N3, "grid")
+        with torch.cuda.device(self.device):
+            _check(lib().nufft_spread(self._h, pc, pg), "nufft_spread")
+        return g
+
+    def interp(self, grid: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        N1, N2, N3 = self.N
+        c = self._out(out, (self.Np,), grid)
+        pg = _ptr(grid, self.cplx, 8 * N1 * N2 * N3, "grid")
+        pc = _ptr(c, self.cplx, self.Np, "c")
+        with torch.cuda.device(self.device):
+            _check(lib().nufft_interp(self._h, pg, pc), "nufft_interp")
+        return c
