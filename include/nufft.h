@@ -55,7 +55,7 @@ enum {
     NUFFT_OK = 0,
     NUFFT_WARN_EPS_CLAMPED = 1, /* eps outside [1e-15, 1e-1] (fp64) / [1e-7, 1e-1] (fp32): clamped */
     NUFFT_ERR_ARG = 2,          /* null handle / pointer, bad enum, bad option                      */
-    NUFFT_ERR_MODES = 3,        /* some N_d odd, < 2, or 2 N_d < w                                   */
+    NUFFT_ERR_MODES = 3,        /* some N_d odd, < 2, or 2 N_d < w + 3                               */
     NUFFT_ERR_NPTS = 4,         /* Np < 0 or Np >= 2^31 on one GPU                                  */
     NUFFT_ERR_NOT_SET = 5,      /* execute / spread / interp before setpts                           */
     NUFFT_ERR_ALLOC = 6,        /* device allocation failed                                          */
@@ -71,7 +71,7 @@ typedef struct {
     void* stream;      /* cudaStream_t for every call of the plan; NULL = the legacy default stream */
     void* comm;        /* NULL = single GPU; else a communicator from nufft_comm_init (slab mode)    */
     int points_owned;  /* distributed: 1 = caller guarantees each point lies in this rank's z-slab   */
-    int tile[3];       /* bin / tile edge in fine cells per axis; 0 = built-in table by w            */
+    int tile[3];       /* bin edge T_d (fine cells); 0 = built-in table by w; T_d + w + 2 <= 2 N_d  */
     int timing;        /* 1 = record per-stage CUDA events (read back by nufft_get_info)              */
     int reserved[7];
 } nufft_opts;
@@ -97,7 +97,7 @@ typedef struct {
 int nufft_default_opts(nufft_opts* o);
 
 /* Create a plan (all precomputation "once during initialization").
- * N1, N2, N3: modes per axis (even, >= 2, 2 N_d >= w).  iflag: sign of the type-1
+ * N1, N2, N3: modes per axis (even, >= 2, 2 N_d >= w + 3).  iflag: sign of the type-1
  * exponent (-1 reproduces Eq. 1); type 2 uses -iflag.  eps: requested relative
  * l2 tolerance.  precision: NUFFT_F32 or NUFFT_F64.  opts may be NULL (defaults).
  * Host: computes w, beta, the deconvolution factors p_d(n) = 2 / (w phihat(pi n w / nf_d))

@@ -1,0 +1,132 @@
+// device_util.cuh -- device helpers shared by the spread / interp kernels:
+// the ES window, periodic index wrap, and the sm_90+/sm_100a bulk-async (TMA
+// engine) copy / reduce primitives with their mbarrier plumbing.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace nufft {
+namespace dev {
+
+// ES window:  phi(z) = exp(beta (sqrt(1 - z^2) - 1)) for |z| <= 1
+// (the endpoint is inside the support, reading R5), 0 otherwise.
+template <typename T> __device__ __forceinline__ T es_weight(T zz, T beta);
+template <> __device__ __forceinline__ double es_weight<double>(double zz, double beta) {
+    const double t = 1.0 - zz * zz;
+    return t >= 0.0 ? exp(beta * (sqrt(t) - 1.0)) : 0.0;
+}
+template <> __device__ __forceinline__ float es_weight<float>(float zz, float beta) {
+    const float t = 1.0f - zz * zz;
+    return t >= 0.0f ? expf(beta * (sqrtf(t) - 1.0f)) : 0.0f;
+}
+
+// one conditional step each way: valid for -n <= i < 2n (the plan guarantees T + w <= nf)
+__device__ __forceinline__ int wrap1(int i, int n) {
+    i += i < 0 ? n : 0;
+    return i >= n ? i - n : i;
+}
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+
+// ---- mbarrier (transaction-count barrier for bulk copies)
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+                 : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// ---- 1D bulk copy global -> shared, completion counted on an mbarrier (UBLKCP)
+__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, unsigned bytes,
+                                         uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst_smem)),
+        "l"(src_gmem), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
+// ---- 1D bulk reduction shared -> global (UBLKRED ... ADD): dst[i] += src[i]
+__device__ __forceinline__ void bulk_red_add(float* dst_gmem, const void* src_smem,
+                                             unsigned bytes) {
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(
+                     dst_gmem),
+                 "r"(smem_addr(src_smem)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_red_add(double* dst_gmem, const void* src_smem,
+                                             unsigned bytes) {
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(
+                     dst_gmem),
+                 "r"(smem_addr(src_smem)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+// generic-proxy shared-memory writes -> visible to the async (bulk) proxy
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// Tile x-geometry shared by spread and interp.  Bulk copies need 16-byte
+// aligned rows: fp64 complex cells are 16 bytes, so any origin works (pitch =
+// T + w); fp32 complex cells are 8 bytes, so the subgrid row starts at an EVEN
+// global x and has an even pitch, round_up_even(T + w + 1).
+struct TileX {
+    int gx0;    // global x of smem column 0 (may be negative: periodic)
+    int shift;  // smem column of the nominal tile origin bx*T - w/2 (0 or 1)
+    int pitch;  // smem row length in cells
+};
+template <int CELL_BYTES>
+__host__ __device__ __forceinline__ int tile_pitch(int T, int W) {
+    return CELL_BYTES >= 16 ? T + W : ((T + W + 2) & ~1);
+}
+template <int CELL_BYTES>
+__device__ __forceinline__ TileX tile_x(int bx, int T, int W) {
+    const int ox = bx * T - W / 2;
+    TileX t;
+    t.shift = CELL_BYTES >= 16 ? 0 : (ox & 1);
+    t.gx0 = ox - t.shift;
+    t.pitch = tile_pitch<CELL_BYTES>(T, W);
+    return t;
+}
+
+// Split a periodic row [gx0, gx0 + len) of a row of length nf into at most two
+// contiguous segments; returns the count.  seg_g = global start, seg_s = smem
+// offset, seg_n = length (cells).  Requires -nf <= gx0 and gx0 + len <= 2 nf.
+__device__ __forceinline__ int row_segments(int gx0, int len, int nf, int seg_g[2], int seg_s[2],
+                                            int seg_n[2]) {
+    if (gx0 < 0) {
+        seg_g[0] = gx0 + nf; seg_s[0] = 0; seg_n[0] = -gx0;
+        seg_g[1] = 0; seg_s[1] = -gx0; seg_n[1] = len + gx0;
+        return 2;
+    }
+    if (gx0 + len > nf) {
+        seg_g[0] = gx0; seg_s[0] = 0; seg_n[0] = nf - gx0;
+        seg_g[1] = 0; seg_s[1] = nf - gx0; seg_n[1] = gx0 + len - nf;
+        return 2;
+    }
+    seg_g[0] = gx0; seg_s[0] = 0; seg_n[0] = len;
+    return 1;
+}
+
+}  // namespace dev
+}  // namespace nufft

@@ -64,6 +64,8 @@ template <typename T>
 cudaError_t launch_interp(const Geom& g, const PtsView<T>& p, int64_t nbins,
                           const typename Cx<T>::type* grid, typename Cx<T>::type* c, double beta,
                           cudaStream_t s);
+template <typename T> size_t spread_smem_bytes(const Geom& g);
+template <typename T> size_t interp_smem_bytes(const Geom& g);
 // elementwise.cu
 template <typename T>
 cudaError_t launch_truncate_deconv(const typename Cx<T>::type* grid, const int64_t nf[3],

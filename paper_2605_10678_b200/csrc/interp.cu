@@ -2,37 +2,41 @@
 //
 // "Sorted interpolation" taken to its B200 form: one CTA per
 // bin stages the bin's (T + w)^3 subgrid from the periodic fine grid into
-// shared memory once (coalesced wrapped loads along x rows), then every point
-// of the bin gathers its w^3 stencil from shared memory.
+// shared memory once, with the bulk-async (TMA) engine: one
+// cp.async.bulk.shared::cta.global (SASS UBLKCP) per contiguous row segment,
+// all completing on a single mbarrier transaction count; rows that cross the
+// periodic boundary split into two segments.  Every point of the bin then
+// gathers its w^3 stencil from shared memory, so each grid cell is read from
+// HBM about ((T + w) / T)^3 times per transform instead of w^3 / (points per
+// cell) times as in direct interpolation.
 //
-// Per point (one warp): lanes 0..3w-1 evaluate the 3w ES weights (separability,
-// PAPER.md:193-196) into a per-warp buffer; the 32 lanes then cover the w x w
-// (x, y) columns, each summing its w z-cells against the z weights, scale by
-// wx * wy, and a shuffle reduction produces c_j, written to the caller's order
-// (c[perm[slot]], "reported in input particle order").
+// Points are handled in chunks of 32 per warp (the bin split evenly over the
+// warps): lane l loads point l's sorted record (coalesced) and evaluates its
+// 3w ES weights in registers (separability; phi direct,
+// PAPER.md:176), parking them in a per-warp shared buffer.  The warp then
+// walks the 32 points: lane slots cover the w x w (x, y) columns of the
+// stencil, each sums its w z-cells against wz, scales by wx*wy, and a shuffle
+// reduction yields c_j, written in the caller's order (c[perm[slot]]).
+#include "device_util.cuh"
 #include "internal.cuh"
 
 namespace nufft {
 
 namespace {
 
+using namespace dev;
+
 constexpr int kInterpThreads = 256;
+constexpr int kInterpWarps = kInterpThreads / 32;
 
-template <typename T> __device__ __forceinline__ T es_weight(T zz, T beta);
-template <> __device__ __forceinline__ double es_weight<double>(double zz, double beta) {
-    const double t = 1.0 - zz * zz;
-    return t >= 0.0 ? exp(beta * (sqrt(t) - 1.0)) : 0.0;
-}
-template <> __device__ __forceinline__ float es_weight<float>(float zz, float beta) {
-    const float t = 1.0f - zz * zz;
-    return t >= 0.0f ? expf(beta * (sqrtf(t) - 1.0f)) : 0.0f;
-}
-
-__device__ __forceinline__ int64_t wrap_idx(int64_t i, int64_t n) {
-    while (i < 0) i += n;
-    while (i >= n) i -= n;
-    return i;
-}
+template <typename T, int W>
+struct InterpSmem {
+    using C = typename Cx<T>::type;
+    static constexpr int WS = 3 * W + 1;  // per-point weight stride (odd: fewer bank conflicts)
+    static size_t bytes(int ncell) {
+        return (size_t)ncell * sizeof(C) + (size_t)kInterpWarps * 32 * WS * sizeof(T) + 16;
+    }
+};
 
 template <typename T, int W>
 __global__ void __launch_bounds__(kInterpThreads, 2)
@@ -40,117 +44,179 @@ __global__ void __launch_bounds__(kInterpThreads, 2)
                        typename Cx<T>::type* __restrict__ out, T beta) {
     using C = typename Cx<T>::type;
     constexpr int NQ = (W * W + 31) / 32;
+    constexpr int WS = InterpSmem<T, W>::WS;
+    constexpr int NW = kInterpWarps;
     extern __shared__ __align__(16) unsigned char smem[];
 
     const int b = blockIdx.x;
     const uint32_t beg = p.offset[b], end = p.offset[b + 1];
     if (beg == end) return;
 
-    const int Ex = g.T[0] + W, Ey = g.T[1] + W, Ez = g.T[2] + W;
-    const int ncell = Ex * Ey * Ez;
+    const int bx = b % g.nb[0], by = (b / g.nb[0]) % g.nb[1], bz = b / (g.nb[0] * g.nb[1]);
+    const TileX tx = tile_x<sizeof(C)>(bx, g.T[0], W);
+    const int Ey = g.T[1] + W, Ez = g.T[2] + W;
+    const int pitch = tx.pitch, plane = pitch * Ey, ncell = plane * Ez;
     C* tile = reinterpret_cast<C*>(smem);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int nwarps = blockDim.x >> 5;
-    T* wb = reinterpret_cast<T*>(tile + ncell) + warp * 3 * W;  // per-warp weights
+    T* wb = reinterpret_cast<T*>(tile + ncell) + warp * 32 * WS;  // [32][WS] per warp
+    uint64_t* bar = reinterpret_cast<uint64_t*>(
+        (reinterpret_cast<uintptr_t>(reinterpret_cast<T*>(tile + ncell) + NW * 32 * WS) + 15) &
+        ~(uintptr_t)15);
 
-    // ---- stage the subgrid (wrapped, coalesced along x rows)
-    const int bx = b % g.nb[0], by = (b / g.nb[0]) % g.nb[1], bz = b / (g.nb[0] * g.nb[1]);
-    const int64_t ox = (int64_t)bx * g.T[0] - W / 2;
-    const int64_t oy = (int64_t)by * g.T[1] - W / 2;
-    const int64_t oz = (int64_t)bz * g.T[2] - W / 2;
-    for (int i = threadIdx.x; i < ncell; i += blockDim.x) {
-        const int cx = i % Ex, cy = (i / Ex) % Ey, cz = i / (Ex * Ey);
-        const int64_t gx = wrap_idx(ox + cx, g.nf[0]);
-        const int64_t gy = wrap_idx(oy + cy, g.nf[1]);
-        const int64_t gz = wrap_idx(oz + cz, g.nz_loc);
-        tile[i] = grid[gx + g.nf[0] * (gy + g.nf[1] * gz)];
+    // ---- stage the subgrid with bulk copies (one mbarrier transaction)
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        mbar_arrive_expect_tx(bar, (unsigned)(ncell * sizeof(C)));
     }
     __syncthreads();
+    {
+        const int oy = by * g.T[1] - W / 2, oz = bz * g.T[2] - W / 2;
+        const int nfx = (int)g.nf[0], nfy = (int)g.nf[1], nfz = (int)g.nz_loc;
+        int sg[2], ss[2], sn[2];
+        const int nseg = row_segments(tx.gx0, pitch, nfx, sg, ss, sn);
+        for (int r = threadIdx.x; r < Ey * Ez; r += kInterpThreads) {
+            const int cz = r / Ey, cy = r - cz * Ey;
+            const int gy = wrap1(oy + cy, nfy), gz = wrap1(oz + cz, nfz);
+            const C* grow = grid + (int64_t)nfx * ((int64_t)gz * nfy + gy);
+            C* trow = tile + r * pitch;
+            for (int k = 0; k < nseg; ++k)
+                bulk_g2s(trow + ss[k], grow + sg[k], (unsigned)(sn[k] * sizeof(C)), bar);
+        }
+    }
 
-    int qx[NQ], qy[NQ];
+    int qoff[NQ], qx[NQ], qy[NQ];
+    bool qok[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
-        const int e = lane + 32 * q;
-        qx[q] = e % W;
-        qy[q] = e < W * W ? e / W : -1;
+        const int s = lane + 32 * q;
+        qok[q] = s < W * W;
+        qx[q] = qok[q] ? s % W : 0;
+        qy[q] = qok[q] ? s / W : 0;
+        qoff[q] = qy[q] * pitch + qx[q];
     }
     const T two_over_w = (T)2 / (T)W;
-    const int plane = Ex * Ey;
+    const uint32_t n = end - beg;
+    const uint32_t wbeg = beg + (uint32_t)(((uint64_t)n * warp) / NW);
+    const uint32_t wend = beg + (uint32_t)(((uint64_t)n * (warp + 1)) / NW);
+    bool staged = false;
 
-    for (uint32_t slot = beg + warp; slot < end; slot += nwarps) {
-        if (lane < 3 * W) {
-            const int d = lane / W, k = lane - d * W;
-            const T dd = d == 0 ? p.dx[slot] : (d == 1 ? p.dy[slot] : p.dz[slot]);
-            wb[lane] = es_weight<T>(((T)k - dd) * two_over_w, beta);
+    for (uint32_t c0 = wbeg; c0 < wend; c0 += 32) {
+        // ---- lane l: record + 3w weights of point c0 + l (overlaps the tile load)
+        const uint32_t slot = c0 + lane;
+        uint32_t my_perm = 0;
+        int my_base = 0;
+        if (slot < wend) {
+            const T d3[3] = {p.dx[slot], p.dy[slot], p.dz[slot]};
+            const uint32_t la = p.la[slot];
+            my_perm = p.perm[slot];
+            my_base = (int)(((la >> 16) * Ey + ((la >> 8) & 0xff)) * pitch + (la & 0xff)) +
+                      tx.shift;
+            T* wl = wb + lane * WS;
+#pragma unroll
+            for (int d = 0; d < 3; ++d)
+#pragma unroll
+                for (int k = 0; k < W; ++k)
+                    wl[d * W + k] = es_weight<T>(((T)k - d3[d]) * two_over_w, beta);
         }
-        const uint32_t la = p.la[slot];
+        if (!staged) {
+            mbar_wait(bar, 0);
+            staged = true;
+        }
         __syncwarp();
-        const int lx = la & 0xff, ly = (la >> 8) & 0xff, lz = la >> 16;
-        T ar = 0, ai = 0;
+        const int np = (int)min(32u, wend - c0);
+        for (int j = 0; j < np; ++j) {
+            const int base = __shfl_sync(0xffffffffu, my_base, j);
+            const T* wj = wb + j * WS;
+            T ar = 0, ai = 0;
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-            if (qy[q] >= 0) {
-                const C* col = tile + lz * plane + (ly + qy[q]) * Ex + lx + qx[q];
-                T sr = 0, si = 0;
+            for (int q = 0; q < NQ; ++q) {
+                if (qok[q]) {
+                    const C* col = tile + base + qoff[q];
+                    T sr = 0, si = 0;
 #pragma unroll
-                for (int k = 0; k < W; ++k) {
-                    const C v = col[k * plane];
-                    const T wz = wb[2 * W + k];
-                    sr += v.x * wz;
-                    si += v.y * wz;
+                    for (int k = 0; k < W; ++k) {
+                        const C v = col[k * plane];
+                        const T wz = wj[2 * W + k];
+                        sr += v.x * wz;
+                        si += v.y * wz;
+                    }
+                    const T wxy = wj[qx[q]] * wj[W + qy[q]];
+                    ar += sr * wxy;
+                    ai += si * wxy;
                 }
-                const T wxy = wb[qx[q]] * wb[W + qy[q]];
-                ar += sr * wxy;
-                ai += si * wxy;
             }
-        }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            ar += __shfl_xor_sync(0xffffffffu, ar, o);
-            ai += __shfl_xor_sync(0xffffffffu, ai, o);
+            for (int o = 16; o > 0; o >>= 1) {
+                ar += __shfl_xor_sync(0xffffffffu, ar, o);
+                ai += __shfl_xor_sync(0xffffffffu, ai, o);
+            }
+            if (lane == j) out[my_perm] = C{ar, ai};
         }
-        if (lane == 0) out[p.perm[slot]] = C{ar, ai};
         __syncwarp();
     }
+    // a warp without points must not exit before the bulk copies into this CTA's
+    // shared memory have landed
+    if (!staged) mbar_wait(bar, 0);
+}
+
+template <typename T, int W>
+size_t smem_w(const Geom& g) {
+    using C = typename Cx<T>::type;
+    return InterpSmem<T, W>::bytes(tile_pitch<sizeof(C)>(g.T[0], W) * (g.T[1] + W) *
+                                   (g.T[2] + W));
 }
 
 template <typename T, int W>
 cudaError_t launch_w(const Geom& g, const PtsView<T>& p, int64_t nbins,
                      const typename Cx<T>::type* grid, typename Cx<T>::type* c, double beta,
                      cudaStream_t s) {
-    using C = typename Cx<T>::type;
-    const size_t ncell = (size_t)(g.T[0] + W) * (g.T[1] + W) * (g.T[2] + W);
-    const size_t smem = ncell * sizeof(C) + (size_t)(kInterpThreads / 32) * 3 * W * sizeof(T);
+    const size_t smem = smem_w<T, W>(g);
     auto kern = interp_tile_kernel<T, W>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
-    if (e != cudaSuccess) return e;
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return e;
+    }
     if (nbins > 0) kern<<<(unsigned)nbins, kInterpThreads, smem, s>>>(g, p, grid, c, (T)beta);
     return cudaGetLastError();
 }
 
 }  // namespace
 
+#define NUFFT_W_SWITCH(CALL)                                                              \
+    switch (g.w) {                                                                        \
+        case 2: return CALL(2); case 3: return CALL(3); case 4: return CALL(4);          \
+        case 5: return CALL(5); case 6: return CALL(6); case 7: return CALL(7);          \
+        case 8: return CALL(8); case 9: return CALL(9); case 10: return CALL(10);        \
+        case 11: return CALL(11); case 12: return CALL(12); case 13: return CALL(13);    \
+        case 14: return CALL(14); case 15: return CALL(15); case 16: return CALL(16);    \
+        default: break;                                                                   \
+    }
+
 template <typename T>
 cudaError_t launch_interp(const Geom& g, const PtsView<T>& p, int64_t nbins,
                           const typename Cx<T>::type* grid, typename Cx<T>::type* c, double beta,
                           cudaStream_t s) {
-    switch (g.w) {
-#define NUFFT_W_CASE(WW) \
-    case WW:             \
-        return launch_w<T, WW>(g, p, nbins, grid, c, beta, s);
-        NUFFT_W_CASE(2) NUFFT_W_CASE(3) NUFFT_W_CASE(4) NUFFT_W_CASE(5) NUFFT_W_CASE(6)
-        NUFFT_W_CASE(7) NUFFT_W_CASE(8) NUFFT_W_CASE(9) NUFFT_W_CASE(10) NUFFT_W_CASE(11)
-        NUFFT_W_CASE(12) NUFFT_W_CASE(13) NUFFT_W_CASE(14) NUFFT_W_CASE(15) NUFFT_W_CASE(16)
-#undef NUFFT_W_CASE
-        default:
-            return cudaErrorInvalidValue;
-    }
+#define CALL(WW) launch_w<T, WW>(g, p, nbins, grid, c, beta, s)
+    NUFFT_W_SWITCH(CALL)
+#undef CALL
+    return cudaErrorInvalidValue;
+}
+
+template <typename T>
+size_t interp_smem_bytes(const Geom& g) {
+#define CALL(WW) smem_w<T, WW>(g)
+    NUFFT_W_SWITCH(CALL)
+#undef CALL
+    return 0;
 }
 
 template cudaError_t launch_interp<float>(const Geom&, const PtsView<float>&, int64_t,
                                           const float2*, float2*, double, cudaStream_t);
 template cudaError_t launch_interp<double>(const Geom&, const PtsView<double>&, int64_t,
                                            const double2*, double2*, double, cudaStream_t);
+template size_t interp_smem_bytes<float>(const Geom&);
+template size_t interp_smem_bytes<double>(const Geom&);
 
 }  // namespace nufft

@@ -11,6 +11,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -243,7 +244,7 @@ int default_tile(int w, int prec, int64_t nf) {
     int t = edge - w;
     if (t < 4) t = 4;
     if (t > 64) t = 64;
-    if (t > nf) t = (int)nf;
+    if (t > nf - w - 2) t = (int)(nf - w - 2);  // T + w + 2 <= nf: one-step periodic wraps, <= 2 row segments
     return t;
 }
 
@@ -343,7 +344,7 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
     int status = select_width(eps, precision, &p->w, &p->beta, &p->eps);
     const int64_t Nv[3] = {N1, N2, N3};
     for (int d = 0; d < 3; ++d) {
-        if (Nv[d] < 2 || (Nv[d] & 1) || 2 * Nv[d] < p->w) {
+        if (Nv[d] < 2 || (Nv[d] & 1) || 2 * Nv[d] < p->w + 3) {
             delete p;
             return NUFFT_ERR_MODES;
         }
@@ -362,7 +363,7 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
     for (int d = 0; d < 3; ++d) {
         g.nf[d] = p->nf[d];
         int t = o.tile[d] > 0 ? o.tile[d] : default_tile(p->w, precision, p->nf[d]);
-        if (t > 255 || t > p->nf[d]) {
+        if (t < 1 || t > 255 || t + p->w + 2 > p->nf[d]) {
             delete p;
             return NUFFT_ERR_ARG;
         }
@@ -376,6 +377,25 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
     g.nz_loc = p->nf[2];
     p->nbins = (int64_t)g.nb[0] * g.nb[1] * g.nb[2];
 
+    // the (T + w)^3 subgrid (+ staging) of the spread / interp kernels must fit in
+    // the opt-in shared memory of one CTA
+    {
+        int dev = 0, smem_max = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) !=
+            cudaSuccess) {
+            cudaGetLastError();
+            delete p;
+            return NUFFT_ERR_CUDA;
+        }
+        const size_t need = precision == NUFFT_F64
+                                ? std::max(spread_smem_bytes<double>(g), interp_smem_bytes<double>(g))
+                                : std::max(spread_smem_bytes<float>(g), interp_smem_bytes<float>(g));
+        if (need > (size_t)smem_max) {
+            delete p;
+            return NUFFT_ERR_ARG;
+        }
+    }
     int st = NUFFT_OK;
     // deconvolution factors p_d(n) = 2 / (w phihat(pi n w / nf_d)) (R6)
     for (int d = 0; d < 3 && !st; ++d) {
@@ -425,6 +445,7 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
 }
 
 int nufft_setpts(nufft_handle p, int64_t Np, const void* x, const void* y, const void* z) {
+    cudaGetLastError();  // a stale non-sticky error of another caller is not ours
     if (!p) return NUFFT_ERR_ARG;
     if (Np < 0 || Np >= (int64_t)1 << 31) return NUFFT_ERR_NPTS;
     if (Np > 0 && (!x || !y || !z)) return NUFFT_ERR_ARG;
@@ -476,6 +497,7 @@ int nufft_setpts(nufft_handle p, int64_t Np, const void* x, const void* y, const
 }
 
 int nufft_execute_type1(nufft_handle p, const void* c, void* fk) {
+    cudaGetLastError();  // a stale non-sticky error of another caller is not ours
     if (!p || !fk || (!c && p->Np > 0)) return NUFFT_ERR_ARG;
     if (p->Np < 0) return NUFFT_ERR_NOT_SET;
     int st;
@@ -507,6 +529,7 @@ int nufft_execute_type1(nufft_handle p, const void* c, void* fk) {
 }
 
 int nufft_execute_type2(nufft_handle p, const void* fk, void* c) {
+    cudaGetLastError();  // a stale non-sticky error of another caller is not ours
     if (!p || !fk || (!c && p->Np > 0)) return NUFFT_ERR_ARG;
     if (p->Np < 0) return NUFFT_ERR_NOT_SET;
     int st;
@@ -536,6 +559,7 @@ int nufft_execute_type2(nufft_handle p, const void* fk, void* c) {
 }
 
 int nufft_spread(nufft_handle p, const void* c, void* grid) {
+    cudaGetLastError();  // a stale non-sticky error of another caller is not ours
     if (!p || !grid || (!c && p->Np > 0)) return NUFFT_ERR_ARG;
     if (p->Np < 0) return NUFFT_ERR_NOT_SET;
     int st;
@@ -550,6 +574,7 @@ int nufft_spread(nufft_handle p, const void* c, void* grid) {
 }
 
 int nufft_interp(nufft_handle p, const void* grid, void* c) {
+    cudaGetLastError();  // a stale non-sticky error of another caller is not ours
     if (!p || !grid || (!c && p->Np > 0)) return NUFFT_ERR_ARG;
     if (p->Np < 0) return NUFFT_ERR_NOT_SET;
     int st;

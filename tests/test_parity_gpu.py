@@ -148,11 +148,14 @@ def test_custom_and_ragged_tiles(nb):
     x, y, z = (np64(p) for p in pts)
     o1 = oracle.type1(x, y, z, np64(c), N, eps)
     o2 = oracle.type2(x, y, z, np64(fk), eps)
-    for tile in [(4, 4, 4), (7, 9, 5), (16, 8, 4), (64, 64, 64)]:
+    for tile in [(4, 4, 4), (7, 9, 5), (16, 8, 4), (32, 12, 3)]:
         plan, g1, g2 = run_pair(nb, N, eps, "f64", pts, c, fk, tile=tile)
         assert tuple(plan.info()["tile"]) == tile
         assert oracle.rel_l2(g1, o1) <= 1e-10, tile
         assert oracle.rel_l2(g2, o2) <= 1e-10, tile
+    # a subgrid that cannot fit in one CTA's shared memory is refused at plan time
+    with pytest.raises(nb.NufftError):
+        nb.Plan(N, eps, tile=(64, 64, 64))
 
 
 def test_edge_cases(nb):
