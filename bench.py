@@ -170,7 +170,8 @@ def run_ours(args, cfg):
 
     pts, c, fk = make_inputs(cfg, rank, device)
     N, Np = cfg["N"], cfg["Np"]
-    plan = nb.Plan(N, cfg["eps"], precision=cfg["prec"], timing=True, device=device)
+    plan = nb.Plan(N, cfg["eps"], precision=cfg["prec"], timing=True, device=device,
+                   tile=args.tile)
     c2 = torch.empty(Np, dtype=c.dtype, device=device)
     fk_out = torch.empty_like(fk)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=device)
@@ -268,6 +269,7 @@ def run_ours(args, cfg):
                                    f"{Np} {cfg['kind']} points, eps={cfg['eps']:g}",
                        "N": list(N), "Np_per_gpu": Np, "eps": cfg["eps"], "w": plan.info()["w"],
                        "precision": cfg["prec"], "points": cfg["kind"],
+                       "tile": plan.info()["tile"],
                        "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU",
                        "l2": "flushed (512 MB write) before every timed step"},
             "stage_ms_median": med,
@@ -354,7 +356,11 @@ def main():
     ap.add_argument("--config", default="c2b", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tile", default=None, help="bin edge T or Tx,Ty,Tz (default: built-in table)")
     args = ap.parse_args()
+    if args.tile is not None:
+        t = [int(v) for v in args.tile.split(",")]
+        args.tile = tuple(t * 3 if len(t) == 1 else t)
     if args.warmup < 3:
         args.warmup = 3
     cfg = CONFIGS[args.config]

@@ -124,33 +124,55 @@ __global__ void __launch_bounds__(kInterpThreads, 2)
         }
         __syncwarp();
         const int np = (int)min(32u, wend - c0);
-        for (int j = 0; j < np; ++j) {
-            const int base = __shfl_sync(0xffffffffu, my_base, j);
-            const T* wj = wb + j * WS;
-            T ar = 0, ai = 0;
+        // four points at a time: independent accumulations, then a transposing
+        // butterfly (offsets 16, 8 split the 4 sums over lane octets, 4, 2, 1 finish)
+        for (int j0 = 0; j0 < np; j0 += 4) {
+            T vr[4], vi[4];
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                if (qok[q]) {
-                    const C* col = tile + base + qoff[q];
-                    T sr = 0, si = 0;
+            for (int g4 = 0; g4 < 4; ++g4) {
+                const int j = j0 + g4;
+                vr[g4] = 0;
+                vi[g4] = 0;
+                if (j < np) {
+                    const int base = __shfl_sync(0xffffffffu, my_base, j);
+                    const T* wj = wb + j * WS;
 #pragma unroll
-                    for (int k = 0; k < W; ++k) {
-                        const C v = col[k * plane];
-                        const T wz = wj[2 * W + k];
-                        sr += v.x * wz;
-                        si += v.y * wz;
+                    for (int q = 0; q < NQ; ++q) {
+                        if (qok[q]) {
+                            const C* col = tile + base + qoff[q];
+                            T sr = 0, si = 0;
+#pragma unroll
+                            for (int k = 0; k < W; ++k) {
+                                const C v = col[k * plane];
+                                const T wz = wj[2 * W + k];
+                                sr += v.x * wz;
+                                si += v.y * wz;
+                            }
+                            const T wxy = wj[qx[q]] * wj[W + qy[q]];
+                            vr[g4] += sr * wxy;
+                            vi[g4] += si * wxy;
+                        }
                     }
-                    const T wxy = wj[qx[q]] * wj[W + qy[q]];
-                    ar += sr * wxy;
-                    ai += si * wxy;
                 }
             }
+            const bool h16 = lane & 16, h8 = lane & 8;
+            T r0 = h16 ? vr[1] : vr[0], r1 = h16 ? vr[3] : vr[2];
+            T i0 = h16 ? vi[1] : vi[0], i1 = h16 ? vi[3] : vi[2];
+            r0 += __shfl_xor_sync(0xffffffffu, h16 ? vr[0] : vr[1], 16);
+            r1 += __shfl_xor_sync(0xffffffffu, h16 ? vr[2] : vr[3], 16);
+            i0 += __shfl_xor_sync(0xffffffffu, h16 ? vi[0] : vi[1], 16);
+            i1 += __shfl_xor_sync(0xffffffffu, h16 ? vi[2] : vi[3], 16);
+            T rr = h8 ? r1 : r0, ii = h8 ? i1 : i0;
+            rr += __shfl_xor_sync(0xffffffffu, h8 ? r0 : r1, 8);
+            ii += __shfl_xor_sync(0xffffffffu, h8 ? i0 : i1, 8);
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                ar += __shfl_xor_sync(0xffffffffu, ar, o);
-                ai += __shfl_xor_sync(0xffffffffu, ai, o);
+            for (int o = 4; o > 0; o >>= 1) {
+                rr += __shfl_xor_sync(0xffffffffu, rr, o);
+                ii += __shfl_xor_sync(0xffffffffu, ii, o);
             }
-            if (lane == j) out[my_perm] = C{ar, ai};
+            const int j = j0 + (h16 ? 1 : 0) + (h8 ? 2 : 0);
+            const uint32_t pj = __shfl_sync(0xffffffffu, my_perm, j & 31);
+            if ((lane & 7) == 0 && j < np) out[pj] = C{rr, ii};
         }
         __syncwarp();
     }

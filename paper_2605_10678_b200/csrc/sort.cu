@@ -12,8 +12,10 @@
 //   k2 scan      : exclusive prefix sum of count[] -> offset[] with warp
 //                  __shfl_up_sync scans, three phases (tile sums, scan of sums,
 //                  tile scans + carry-in).
-//   k3 scatter   : slot = offset[bin] + rank; perm[slot] = j and the sorted
-//                  stencil record (local base la, phase offsets d) for the slot.
+//   k3 scatter   : slot = offset[bin] + rank; perm[slot] = j (one 4-byte write).
+//   k4 records   : in slot order, gather x[perm], y[perm], z[perm] and write the
+//                  sorted stencil record (local base la, phase offsets d)
+//                  coalesced.
 #include "internal.cuh"
 
 namespace nufft {
@@ -170,16 +172,25 @@ __device__ __forceinline__ void local_stencil(double s, int c, int T, int w, int
     *d = ls - a;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kSortThreads) scatter_kernel(
-    Geom g, int64_t Np, const T* __restrict__ x, const T* __restrict__ y,
-    const T* __restrict__ z, const uint32_t* __restrict__ bin_of,
-    const uint32_t* __restrict__ rank_of, const uint32_t* __restrict__ offset,
-    uint32_t* __restrict__ perm, T* __restrict__ dx, T* __restrict__ dy, T* __restrict__ dz,
-    uint32_t* __restrict__ la) {
+__global__ void __launch_bounds__(kSortThreads) scatter_perm_kernel(
+    int64_t Np, const uint32_t* __restrict__ bin_of, const uint32_t* __restrict__ rank_of,
+    const uint32_t* __restrict__ offset, uint32_t* __restrict__ perm) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < Np;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t slot = offset[bin_of[i]] + rank_of[i];
+         i += (int64_t)gridDim.x * blockDim.x)
+        perm[offset[bin_of[i]] + rank_of[i]] = (uint32_t)i;
+}
+
+// Sorted records, written coalesced in slot order (the coordinates are gathered
+// through perm): random 8-byte READS instead of five random partial-sector
+// writes per point.
+template <typename T>
+__global__ void __launch_bounds__(kSortThreads) records_kernel(
+    Geom g, int64_t Np, const T* __restrict__ x, const T* __restrict__ y,
+    const T* __restrict__ z, const uint32_t* __restrict__ perm, T* __restrict__ dx,
+    T* __restrict__ dy, T* __restrict__ dz, uint32_t* __restrict__ la) {
+    for (int64_t slot = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; slot < Np;
+         slot += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t i = perm[slot];
         const double sx = fold_rescale((double)x[i], g.L, g.scale[0], g.nf[0]);
         const double sy = fold_rescale((double)y[i], g.L, g.scale[1], g.nf[1]);
         const double sz = fold_rescale((double)z[i], g.L, g.scale[2], g.nf[2]) - (double)g.z_lo;
@@ -189,7 +200,6 @@ __global__ void __launch_bounds__(kSortThreads) scatter_kernel(
         local_stencil(sy, cell_of(sy, g.nf[1]), g.T[1], g.w, &lay, &ddy);
         local_stencil(sz, cell_of(sz + (double)g.z_lo, g.nf[2]) - (int)g.z_lo, g.T[2], g.w, &laz,
                       &ddz);
-        perm[slot] = (uint32_t)i;
         dx[slot] = (T)ddx;
         dy[slot] = (T)ddy;
         dz[slot] = (T)ddz;
@@ -224,8 +234,10 @@ cudaError_t launch_bin_sort(const Geom& g, int64_t Np, const T* x, const T* y, c
     scan_sums<<<1, kScanThreads, 0, s>>>(blocksum, ntiles);
     scan_tiles<<<(unsigned)ntiles, kScanThreads, 0, s>>>(count, nbins, blocksum, offset);
     if (Np > 0) {
-        scatter_kernel<T><<<grid_for(Np, kSortThreads), kSortThreads, 0, s>>>(
-            g, Np, x, y, z, bin_of, rank_of, offset, perm, dx, dy, dz, la);
+        scatter_perm_kernel<<<grid_for(Np, kSortThreads), kSortThreads, 0, s>>>(
+            Np, bin_of, rank_of, offset, perm);
+        records_kernel<T><<<grid_for(Np, kSortThreads), kSortThreads, 0, s>>>(
+            g, Np, x, y, z, perm, dx, dy, dz, la);
     }
     return cudaGetLastError();
 }

@@ -2,25 +2,24 @@
 //
 // One CTA per bin (tile of T^3 fine cells).  The CTA owns a shared-memory
 // subgrid of (T + w)^3 complex cells ("a shared memory histogram of size
-// prod(T_i + w)").  The bin's sorted points are split evenly
-// over the warps, which then work independently (no CTA barrier between the
-// zero fill and the flush):
+// prod(T_i + w)") and processes the bin's sorted points in
+// batches:
 //
-//   weights  lane l loads point l of a 32-point chunk (sorted record, strength
-//            gathered through perm) and evaluates its 3w ES weights in
-//            registers -- d w evaluations per point thanks to separability
-//            (PAPER.md:193-196), phi evaluated directly --
-//            parked in a per-warp buffer as wx, wy and the complex z-profile
-//            c * wz;
-//   deposit  the warp walks the chunk's points; lane slots cover the w x w
-//            (x, y) columns of the stencil, each adds c wz wx wy into its w
-//            z-cells.  A shared-memory cell update is ONE packed compare-and-
-//            swap of the whole complex value (fp32: 64-bit CAS of (re, im);
-//            fp64: atom.shared.cas.b128).  On sm_100a shared-memory float
-//            atomics are CAS loops anyway (ATOMS.CAST.SPIN), so packing both
-//            components into one CAS halves the atomic count of the paper's
-//            Tiled spread without the per-warp ownership
-//            bookkeeping of its Grid-Parallel variant;
+//   phase A  one thread per point evaluates the 3w ES weights in registers --
+//            d w evaluations per point thanks to separability
+//            (PAPER.md:193-196), phi evaluated directly -- and
+//            stages, per point, the w x w products wx*wy laid out by lane slot
+//            and the complex z-profile c*wz;
+//   phase B  accumulation WITHOUT atomics: warp k owns the subgrid z-planes
+//            {z : z mod NW == k} (absolute ownership, so no barrier or point
+//            order is needed between points); for every point, the warp takes
+//            the planes of the point's stencil that it owns and its 32 lanes
+//            cover the w x w (x, y) cells of each such plane -- one shared
+//            load, two FMAs and one shared store per cell.  No two threads ever
+//            touch the same cell concurrently (the paper's Grid-Parallel
+//            ownership, with its z-split of the stencil across
+//            teams).  On sm_100a shared-memory float atomics are
+//            CAS loops (ATOMS.CAST.SPIN), so ownership beats atomics;
 //   flush    each subgrid row is added into the periodic fine grid in HBM by
 //            the bulk-async engine: cp.reduce.async.bulk ... .add.f32/.f64
 //            (SASS UBLKRED), one instruction per contiguous row segment; rows
@@ -36,76 +35,36 @@ namespace {
 
 using namespace dev;
 
-constexpr int kSpreadThreads = 256;
-constexpr int kSpreadWarps = kSpreadThreads / 32;
-// points per warp chunk (fp64 halves it to keep the per-warp buffers small)
-template <typename T> struct Chunk;
-template <> struct Chunk<float> { static constexpr int value = 32; };
-template <> struct Chunk<double> { static constexpr int value = 16; };
-
-// cell += a * s with one packed 64-bit CAS of (re, im); retries are rare
-__device__ __forceinline__ void smem_cas_add(float2* cell, float2 a, float s) {
-    unsigned long long* p = reinterpret_cast<unsigned long long*>(cell);
-    unsigned long long seen = *reinterpret_cast<volatile unsigned long long*>(p);
-    float2 v = *reinterpret_cast<float2*>(&seen);
-    v.x = fmaf(a.x, s, v.x);
-    v.y = fmaf(a.y, s, v.y);
-    unsigned long long old = atomicCAS(p, seen, *reinterpret_cast<unsigned long long*>(&v));
-    while (__builtin_expect(old != seen, 0)) {
-        seen = old;
-        v = *reinterpret_cast<float2*>(&seen);
-        v.x = fmaf(a.x, s, v.x);
-        v.y = fmaf(a.y, s, v.y);
-        old = atomicCAS(p, seen, *reinterpret_cast<unsigned long long*>(&v));
-    }
-}
-
-__device__ __forceinline__ bool cas128(unsigned addr, double2& cur, double nx, double ny) {
-    unsigned long long o0, o1;
-    asm volatile(
-        "{\n\t.reg .b128 cmp, nw, old;\n\t"
-        "mov.b128 cmp, {%2, %3};\n\t"
-        "mov.b128 nw, {%4, %5};\n\t"
-        "atom.shared.cas.b128 old, [%6], cmp, nw;\n\t"
-        "mov.b128 {%0, %1}, old;\n\t}"
-        : "=l"(o0), "=l"(o1)
-        : "l"(__double_as_longlong(cur.x)), "l"(__double_as_longlong(cur.y)),
-          "l"(__double_as_longlong(nx)), "l"(__double_as_longlong(ny)), "r"(addr)
-        : "memory");
-    const bool ok = o0 == (unsigned long long)__double_as_longlong(cur.x) &&
-                    o1 == (unsigned long long)__double_as_longlong(cur.y);
-    cur.x = __longlong_as_double((long long)o0);
-    cur.y = __longlong_as_double((long long)o1);
-    return ok;
-}
-
-__device__ __forceinline__ void smem_cas_add(double2* cell, double2 a, double s) {
-    const unsigned addr = smem_addr(cell);
-    const volatile double* vc = reinterpret_cast<volatile double*>(cell);
-    double2 cur = make_double2(vc[0], vc[1]);
-    bool ok = cas128(addr, cur, fma(a.x, s, cur.x), fma(a.y, s, cur.y));
-    while (__builtin_expect(!ok, 0)) ok = cas128(addr, cur, fma(a.x, s, cur.x), fma(a.y, s, cur.y));
-}
+// warps per CTA: plane owners (compile-time, so plane ownership is a mask, not a modulo)
+constexpr int kSpreadWarps = 4;
+constexpr int kSpreadThreads = 32 * kSpreadWarps;
+// points staged per batch
+template <typename T> struct Batch;
+template <> struct Batch<float> { static constexpr int value = 64; };
+template <> struct Batch<double> { static constexpr int value = 32; };
 
 template <typename T, int W>
 struct SpreadSmem {
     using C = typename Cx<T>::type;
-    static constexpr int CH = Chunk<T>::value;
-    // per point: cwz[W] complex, wx|wy [2W] reals, base int
-    static constexpr size_t per_warp() {
-        return (size_t)CH * W * sizeof(C) + (size_t)CH * 2 * W * sizeof(T) + CH * sizeof(int);
+    static constexpr int B = Batch<T>::value;
+    static constexpr int NQ = (W * W + 31) / 32;
+    // per point: wxy[NQ*32] reals (by lane slot), cwz[W] complex, strength, 1D weights
+    // [3][W] reals, base + lz ints
+    static constexpr size_t batch_bytes() {
+        return (size_t)B * NQ * 32 * sizeof(T) + (size_t)B * W * sizeof(C) + (size_t)B * sizeof(C) +
+               (size_t)B * 3 * W * sizeof(T) + (size_t)B * 2 * sizeof(int);
     }
-    static size_t bytes(int ncell) { return (size_t)ncell * sizeof(C) + kSpreadWarps * per_warp(); }
+    static size_t bytes(int ncell) { return (size_t)ncell * sizeof(C) + batch_bytes(); }
 };
 
 template <typename T, int W>
-__global__ void __launch_bounds__(kSpreadThreads, 2)
+__global__ void __launch_bounds__(kSpreadThreads)
     spread_tile_kernel(Geom g, PtsView<T> p, const typename Cx<T>::type* __restrict__ c,
                        typename Cx<T>::type* __restrict__ grid, T beta) {
     using C = typename Cx<T>::type;
     using S = SpreadSmem<T, W>;
-    constexpr int CH = S::CH;
-    constexpr int NQ = (W * W + 31) / 32;
+    constexpr int B = S::B;
+    constexpr int NQ = S::NQ;
     constexpr int NW = kSpreadWarps;
     extern __shared__ __align__(16) unsigned char smem[];
 
@@ -118,74 +77,83 @@ __global__ void __launch_bounds__(kSpreadThreads, 2)
     const int Ey = g.T[1] + W, Ez = g.T[2] + W;
     const int pitch = tx.pitch, plane = pitch * Ey, ncell = plane * Ez;
     C* tile = reinterpret_cast<C*>(smem);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned char* wsm = smem + (size_t)ncell * sizeof(C) + warp * S::per_warp();
-    C* cwz = reinterpret_cast<C*>(wsm);                       // [CH][W]
-    T* wxy1 = reinterpret_cast<T*>(cwz + CH * W);            // [CH][2W]: wx | wy
-    int* sbase = reinterpret_cast<int*>(wxy1 + CH * 2 * W);  // [CH]
+    T* swxy = reinterpret_cast<T*>(tile + ncell);          // [B][NQ*32]
+    C* scwz = reinterpret_cast<C*>(swxy + B * NQ * 32);   // [B][W]
+    C* scv = scwz + B * W;                                 // [B] strengths
+    T* sw1d = reinterpret_cast<T*>(scv + B);               // [B][3][W] 1D weights
+    int* sbase = reinterpret_cast<int*>(sw1d + B * 3 * W); // [B]
+    int* slz = sbase + B;                                  // [B]
 
     for (int i = threadIdx.x; i < ncell; i += kSpreadThreads) tile[i] = C{0, 0};
 
-    int qoff[NQ], qx[NQ], qy[NQ];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int qoff[NQ];
     bool qok[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
         const int s = lane + 32 * q;
         qok[q] = s < W * W;
-        qx[q] = qok[q] ? s % W : 0;
-        qy[q] = qok[q] ? s / W : 0;
-        qoff[q] = qy[q] * pitch + qx[q];
+        qoff[q] = qok[q] ? (s / W) * pitch + (s % W) : 0;
     }
     const T two_over_w = (T)2 / (T)W;
-    // even split of the bin's points over the warps
-    const uint32_t n = end - beg;
-    const uint32_t wbeg = beg + (uint32_t)(((uint64_t)n * warp) / NW);
-    const uint32_t wend = beg + (uint32_t)(((uint64_t)n * (warp + 1)) / NW);
-    __syncthreads();
 
-    for (uint32_t c0 = wbeg; c0 < wend; c0 += CH) {
-        const int np = (int)min((uint32_t)CH, wend - c0);
-        // ---- weights: lane l < np owns point c0 + l
-        if (lane < np) {
-            const uint32_t slot = c0 + lane;
-            const T dx = p.dx[slot], dy = p.dy[slot], dz = p.dz[slot];
-            const uint32_t la = p.la[slot];
-            const C cv = c[p.perm[slot]];
-            sbase[lane] = (int)(((la >> 16) * Ey + ((la >> 8) & 0xff)) * pitch + (la & 0xff)) +
-                          tx.shift;
-            T* wl = wxy1 + lane * 2 * W;
-            C* cl = cwz + lane * W;
+    for (uint32_t p0 = beg; p0 < end; p0 += B) {
+        const int n = (int)min((uint32_t)B, end - p0);
+        __syncthreads();  // previous batch consumed (first round: tile zeroed)
+        // ---- phase A1: one thread per (point, axis): w ES weights; strength; base
+        for (int t = threadIdx.x; t < 3 * n; t += kSpreadThreads) {
+            const int i = t / 3, d = t - 3 * i;
+            const uint32_t slot = p0 + i;
+            const T dd = d == 0 ? p.dx[slot] : (d == 1 ? p.dy[slot] : p.dz[slot]);
+            T* wd = sw1d + t * W;
 #pragma unroll
-            for (int k = 0; k < W; ++k) {
-                const T kk = (T)k;
-                wl[k] = es_weight<T>((kk - dx) * two_over_w, beta);
-                wl[W + k] = es_weight<T>((kk - dy) * two_over_w, beta);
-                const T wz = es_weight<T>((kk - dz) * two_over_w, beta);
-                cl[k] = C{cv.x * wz, cv.y * wz};
+            for (int k = 0; k < W; ++k) wd[k] = es_weight<T>(((T)k - dd) * two_over_w, beta);
+            if (d == 2) {
+                const uint32_t la = p.la[slot];
+                const int lz = (int)(la >> 16);
+                sbase[i] = (lz * Ey + (int)((la >> 8) & 0xff)) * pitch + (int)(la & 0xff) + tx.shift;
+                slz[i] = lz;
+                scv[i] = c[p.perm[slot]];
             }
         }
-        __syncwarp();
-        // ---- deposit the chunk's points
-        for (int j = 0; j < np; ++j) {
-            const int base = sbase[j];
-            const T* wl = wxy1 + j * 2 * W;
-            const C* cl = cwz + j * W;
+        __syncthreads();
+        // ---- phase A2: wx*wy by lane slot, c*wz
+        for (int e = threadIdx.x; e < n * NQ * 32; e += kSpreadThreads) {
+            const int i = e / (NQ * 32), s = e - i * (NQ * 32);
+            const T* wd = sw1d + i * 3 * W;
+            swxy[e] = s < W * W ? wd[W + s / W] * wd[s % W] : (T)0;
+        }
+        for (int e = threadIdx.x; e < n * W; e += kSpreadThreads) {
+            const int i = e / W, k = e - i * W;
+            const T wz = sw1d[i * 3 * W + 2 * W + k];
+            const C cv = scv[i];
+            scwz[e] = C{cv.x * wz, cv.y * wz};
+        }
+        __syncthreads();
+        // ---- phase B: warp-owned z-planes {z : z % NW == warp}
+        for (int i = 0; i < n; ++i) {
+            const int lz = slz[i];
+            int k = (warp - lz) & (NW - 1);  // first owned plane offset in the stencil
+            if (k >= W) continue;
             T wq[NQ];
-            C* cq[NQ];
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                wq[q] = wl[qx[q]] * wl[W + qy[q]];
-                cq[q] = tile + base + qoff[q];
-            }
+            for (int q = 0; q < NQ; ++q) wq[q] = swxy[i * NQ * 32 + lane + 32 * q];
+            const C* cz = scwz + i * W;
+            C* row = tile + sbase[i] + k * plane;
+            for (; k < W; k += NW, row += NW * plane) {
+                const C cv = cz[k];
 #pragma unroll
-            for (int k = 0; k < W; ++k) {
-                const C cz = cl[k];
-#pragma unroll
-                for (int q = 0; q < NQ; ++q)
-                    if (qok[q]) smem_cas_add(cq[q] + k * plane, cz, wq[q]);
+                for (int q = 0; q < NQ; ++q) {
+                    if (qok[q]) {
+                        C* cell = row + qoff[q];
+                        C v = *cell;
+                        v.x += cv.x * wq[q];
+                        v.y += cv.y * wq[q];
+                        *cell = v;
+                    }
+                }
             }
         }
-        __syncwarp();
     }
     fence_proxy_async_smem();
     __syncthreads();

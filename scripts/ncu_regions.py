@@ -6,7 +6,7 @@ ncta = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
 hi = next(i for i, r in enumerate(rows) if "Source" in r and "Instructions Executed" in r)
 h = rows[hi]; si = h.index("Source"); ie = h.index("Instructions Executed")
 ws = h.index("Warp Stall Sampling (All Samples)")
-data = [r for r in rows[hi + 1:] if len(r) > ie]
+data = [r for r in rows[hi + 1:] if len(r) > ie and r[ie].replace(",", "").replace(".", "").isdigit()]
 f = lambda v: float(v.replace(",", "") or 0)
 tot = sum(f(r[ie]) for r in data); tots = sum(f(r[ws]) for r in data)
 regions = []

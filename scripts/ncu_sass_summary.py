@@ -9,7 +9,7 @@ rows = list(csv.reader(open(sys.argv[1])))
 hi = next(i for i, r in enumerate(rows) if "Source" in r and "Instructions Executed" in r)
 h = rows[hi]
 si, ie, ws = h.index("Source"), h.index("Instructions Executed"), h.index("Warp Stall Sampling (All Samples)")
-data = [r for r in rows[hi + 1:] if len(r) > ie and r[si].strip()]
+data = [r for r in rows[hi + 1:] if len(r) > ie and r[si].strip() and r[ie].replace(",", "").replace(".", "").isdigit()]
 f = lambda v: float(v.replace(",", "") or 0)
 tot_i = sum(f(r[ie]) for r in data)
 tot_s = sum(f(r[ws]) for r in data)
