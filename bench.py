@@ -171,7 +171,7 @@ def run_ours(args, cfg):
     pts, c, fk = make_inputs(cfg, rank, device)
     N, Np = cfg["N"], cfg["Np"]
     plan = nb.Plan(N, cfg["eps"], precision=cfg["prec"], timing=True, device=device,
-                   tile=args.tile)
+                   tile=args.tile, spread_warps=args.spread_warps)
     c2 = torch.empty(Np, dtype=c.dtype, device=device)
     fk_out = torch.empty_like(fk)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=device)
@@ -357,6 +357,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--tile", default=None, help="bin edge T or Tx,Ty,Tz (default: built-in table)")
+    ap.add_argument("--spread-warps", type=int, default=0, help="4 or 8 (default: built-in)")
     args = ap.parse_args()
     if args.tile is not None:
         t = [int(v) for v in args.tile.split(",")]

@@ -73,7 +73,8 @@ typedef struct {
     int points_owned;  /* distributed: 1 = caller guarantees each point lies in this rank's z-slab   */
     int tile[3];       /* bin edge T_d (fine cells); 0 = built-in table by w; T_d + w + 2 <= 2 N_d  */
     int timing;        /* 1 = record per-stage CUDA events (read back by nufft_get_info)              */
-    int reserved[7];
+    int spread_warps;  /* warps per spread CTA (z-plane owners): 4 or 8; 0 = built-in choice          */
+    int reserved[6];
 } nufft_opts;
 
 typedef struct {

@@ -28,7 +28,7 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler",
           "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 CU_FLAGS = ARCH + COMMON + ["--expt-relaxed-constexpr", "-Xptxas", "-v"]
 
-SOURCES = ["sort.cu", "spread.cu", "interp.cu", "elementwise.cu", "plan.cpp"]
+SOURCES = ["sort.cu", "spread.cu", "spread_rows.cu", "interp.cu", "elementwise.cu", "plan.cpp"]
 
 
 def _nccl_dirs():

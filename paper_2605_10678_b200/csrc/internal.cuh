@@ -29,20 +29,25 @@ struct Geom {
     double L;           // period
     double scale[3];    // nf / L
     int w;              // kernel width
+    int spread_warps;   // spread kernel: 1 = register rows, 4 / 8 = smem z-plane owners
 };
 
-// Sorted point records written by setpts (SoA, indexed by sorted slot).
-//   perm[i]  : original (caller) index of the point in slot i
-//   d{x,y,z} : ls - la, the stencil phase offset in cells, in [w/2 - 1, w/2]
-//   la[i]    : packed bin-local stencil base (8 bits per axis), la in [0, T]
-// The weight of stencil node k on axis d is phi(2 (k - d_d) / w).
+// Sorted point record written by setpts, one 32-byte (one DRAM sector) AoS
+// record per sorted slot:
+//   d[0..2] : ls - la, the stencil phase offset in cells per axis, in [w/2 - 1, w/2]
+//   la      : packed bin-local stencil base (8 bits per axis), la in [0, T]
+//   perm    : original (caller) index of the point
+// The weight of stencil node k on axis d is phi(2 (k - d[d]) / w).
+template <typename T> struct alignas(32) PtRec {
+    T d[3];
+    uint32_t la;
+    uint32_t perm;
+};
+static_assert(sizeof(PtRec<double>) == 32 && sizeof(PtRec<float>) == 32, "one sector per point");
+
 template <typename T> struct PtsView {
     const uint32_t* offset;  // nbins + 1 bin starts (exclusive scan of counts)
-    const uint32_t* perm;
-    const T* dx;
-    const T* dy;
-    const T* dz;
-    const uint32_t* la;
+    const PtRec<T>* rec;     // Np sorted records
 };
 
 // ---------------------------------------------------------------- kernel launchers
@@ -50,8 +55,8 @@ template <typename T> struct PtsView {
 template <typename T>
 cudaError_t launch_bin_sort(const Geom& g, int64_t Np, const T* x, const T* y, const T* z,
                             uint32_t* count, uint32_t* offset, uint32_t* blocksum,
-                            uint32_t* bin_of, uint32_t* rank_of, uint32_t* perm, T* dx, T* dy,
-                            T* dz, uint32_t* la, int64_t nbins, cudaStream_t s);
+                            uint32_t* bin_of, uint32_t* rank_of, PtRec<T>* rec, int64_t nbins,
+                            cudaStream_t s);
 size_t scan_blocksum_elems(int64_t nbins);
 
 // spread.cu: grid (nf[0] x nf[1] x nz_loc complex, x fastest) += C c
@@ -65,6 +70,13 @@ cudaError_t launch_interp(const Geom& g, const PtsView<T>& p, int64_t nbins,
                           const typename Cx<T>::type* grid, typename Cx<T>::type* c, double beta,
                           cudaStream_t s);
 template <typename T> size_t spread_smem_bytes(const Geom& g);
+// spread_rows.cu: register-row spread (default when w <= 12 and T = 16 - w on every axis)
+bool spread_rows_applies(const Geom& g);
+template <typename T>
+cudaError_t launch_spread_rows(const Geom& g, const PtsView<T>& p, int64_t nbins,
+                               const typename Cx<T>::type* c, typename Cx<T>::type* grid,
+                               double beta, cudaStream_t s);
+template <typename T> size_t spread_rows_smem_bytes(const Geom& g);
 template <typename T> size_t interp_smem_bytes(const Geom& g);
 // elementwise.cu
 template <typename T>

@@ -106,9 +106,10 @@ __global__ void __launch_bounds__(kInterpThreads, 2)
         uint32_t my_perm = 0;
         int my_base = 0;
         if (slot < wend) {
-            const T d3[3] = {p.dx[slot], p.dy[slot], p.dz[slot]};
-            const uint32_t la = p.la[slot];
-            my_perm = p.perm[slot];
+            const PtRec<T> rr = p.rec[slot];
+            const T d3[3] = {rr.d[0], rr.d[1], rr.d[2]};
+            const uint32_t la = rr.la;
+            my_perm = rr.perm;
             my_base = (int)(((la >> 16) * Ey + ((la >> 8) & 0xff)) * pitch + (la & 0xff)) +
                       tx.shift;
             T* wl = wb + lane * WS;

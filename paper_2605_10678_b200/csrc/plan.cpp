@@ -110,11 +110,7 @@ struct nufft_plan_s {
     uint32_t* blocksum = nullptr;
     uint32_t* bin_of = nullptr;
     uint32_t* rank_of = nullptr;
-    uint32_t* perm = nullptr;
-    uint32_t* la = nullptr;
-    void* dx = nullptr;
-    void* dy = nullptr;
-    void* dz = nullptr;
+    void* rec = nullptr;  // Np sorted 32-byte records (PtRec)
 
     // host staging
     void* stage_in = nullptr;
@@ -236,12 +232,12 @@ int finish_output(nufft_plan_s* p, void* dst, const void* dev, size_t bytes, boo
     return NUFFT_OK;
 }
 
-// Default bin edge by width: the (T + w)^3 subgrid of complex cells should stay
-// near 64 KB (fp64: T + w ~ 16, fp32: T + w ~ 20) so that two or more CTAs fit
-// per SM; never below 4 and never larger than the grid.
+// Default bin edge by width (measured on B200, profiles/README.md): fp32 uses the
+// register-row spread, whose subgrid is 16 x 16 x 16 cells (T = 16 - w); fp64 uses
+// the shared-memory z-plane spread with T = 8 up to w = 8 (subgrid <= 16^3 x 16 B
+// = 64 KB), T = 16 - w (>= 4) beyond; never larger than the grid allows.
 int default_tile(int w, int prec, int64_t nf) {
-    const int edge = prec == NUFFT_F64 ? 16 : 20;
-    int t = edge - w;
+    int t = (prec == NUFFT_F64 && w <= 8) ? 8 : 16 - w;
     if (t < 4) t = 4;
     if (t > 64) t = 64;
     if (t > nf - w - 2) t = (int)(nf - w - 2);  // T + w + 2 <= nf: one-step periodic wraps, <= 2 row segments
@@ -252,18 +248,23 @@ template <typename T>
 PtsView<T> pts_view(nufft_plan_s* p) {
     PtsView<T> v;
     v.offset = p->offset;
-    v.perm = p->perm;
-    v.dx = static_cast<const T*>(p->dx);
-    v.dy = static_cast<const T*>(p->dy);
-    v.dz = static_cast<const T*>(p->dz);
-    v.la = p->la;
+    v.rec = static_cast<const PtRec<T>*>(p->rec);
     return v;
 }
 
 int do_spread(nufft_plan_s* p, const void* c_dev, void* grid_dev) {
     CK(cudaMemsetAsync(grid_dev, 0, p->grid_bytes, p->stream));
     StageTimer tm(p, EV_SPREAD);
-    if (p->prec == NUFFT_F64)
+    const bool rows = p->geom.spread_warps == 1;  // register-row kernel (plan checked it applies)
+    if (rows && p->prec == NUFFT_F64)
+        CK(launch_spread_rows<double>(p->geom, pts_view<double>(p), p->nbins,
+                                      static_cast<const double2*>(c_dev),
+                                      static_cast<double2*>(grid_dev), p->beta, p->stream));
+    else if (rows)
+        CK(launch_spread_rows<float>(p->geom, pts_view<float>(p), p->nbins,
+                                     static_cast<const float2*>(c_dev),
+                                     static_cast<float2*>(grid_dev), p->beta, p->stream));
+    else if (p->prec == NUFFT_F64)
         CK(launch_spread<double>(p->geom, pts_view<double>(p), p->nbins,
                                  static_cast<const double2*>(c_dev),
                                  static_cast<double2*>(grid_dev), p->beta, p->stream));
@@ -375,6 +376,21 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
     g.w = p->w;
     g.z_lo = 0;
     g.nz_loc = p->nf[2];
+    // spread kernel: 1 = register rows (needs w <= 12 and T = 16 - w), 4 / 8 = shared-
+    // memory z-plane owners with that many warps; 0 = rows for fp32 when they apply,
+    // else 8 z-plane owners (the faster pair on B200 per precision, profiles/README.md)
+    if (o.spread_warps != 0 && o.spread_warps != 1 && o.spread_warps != 4 &&
+        o.spread_warps != 8) {
+        delete p;
+        return NUFFT_ERR_ARG;
+    }
+    g.spread_warps = o.spread_warps;
+    if (g.spread_warps == 0)
+        g.spread_warps = (precision == NUFFT_F32 && spread_rows_applies(g)) ? 1 : 8;
+    if (g.spread_warps == 1 && !spread_rows_applies(g)) {
+        delete p;
+        return NUFFT_ERR_UNSUPPORTED;
+    }
     p->nbins = (int64_t)g.nb[0] * g.nb[1] * g.nb[2];
 
     // the (T + w)^3 subgrid (+ staging) of the spread / interp kernels must fit in
@@ -388,9 +404,12 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
             delete p;
             return NUFFT_ERR_CUDA;
         }
-        const size_t need = precision == NUFFT_F64
-                                ? std::max(spread_smem_bytes<double>(g), interp_smem_bytes<double>(g))
-                                : std::max(spread_smem_bytes<float>(g), interp_smem_bytes<float>(g));
+        const bool rows = g.spread_warps == 1;
+        const size_t sp = precision == NUFFT_F64
+                              ? (rows ? spread_rows_smem_bytes<double>(g) : spread_smem_bytes<double>(g))
+                              : (rows ? spread_rows_smem_bytes<float>(g) : spread_smem_bytes<float>(g));
+        const size_t need = std::max(sp, precision == NUFFT_F64 ? interp_smem_bytes<double>(g)
+                                                                : interp_smem_bytes<float>(g));
         if (need > (size_t)smem_max) {
             delete p;
             return NUFFT_ERR_ARG;
@@ -454,20 +473,12 @@ int nufft_setpts(nufft_handle p, int64_t Np, const void* x, const void* y, const
     if (Np > p->cap) {
         dev_free(p, (void**)&p->bin_of, 4 * p->cap);
         dev_free(p, (void**)&p->rank_of, 4 * p->cap);
-        dev_free(p, (void**)&p->perm, 4 * p->cap);
-        dev_free(p, (void**)&p->la, 4 * p->cap);
-        dev_free(p, &p->dx, p->real_size * p->cap);
-        dev_free(p, &p->dy, p->real_size * p->cap);
-        dev_free(p, &p->dz, p->real_size * p->cap);
+        dev_free(p, &p->rec, 32 * p->cap);
         p->cap = 0;
         const size_t n = (size_t)Np;
         st = dev_alloc(p, (void**)&p->bin_of, 4 * n);
         if (!st) st = dev_alloc(p, (void**)&p->rank_of, 4 * n);
-        if (!st) st = dev_alloc(p, (void**)&p->perm, 4 * n);
-        if (!st) st = dev_alloc(p, (void**)&p->la, 4 * n);
-        if (!st) st = dev_alloc(p, &p->dx, p->real_size * n);
-        if (!st) st = dev_alloc(p, &p->dy, p->real_size * n);
-        if (!st) st = dev_alloc(p, &p->dz, p->real_size * n);
+        if (!st) st = dev_alloc(p, &p->rec, 32 * n);
         if (st) {
             p->Np = -1;
             return st;
@@ -483,15 +494,12 @@ int nufft_setpts(nufft_handle p, int64_t Np, const void* x, const void* y, const
         CK(launch_bin_sort<double>(p->geom, Np, static_cast<const double*>(xd),
                                    static_cast<const double*>(yd), static_cast<const double*>(zd),
                                    p->count, p->offset, p->blocksum, p->bin_of, p->rank_of,
-                                   p->perm, static_cast<double*>(p->dx),
-                                   static_cast<double*>(p->dy), static_cast<double*>(p->dz),
-                                   p->la, p->nbins, p->stream));
+                                   static_cast<PtRec<double>*>(p->rec), p->nbins, p->stream));
     else
         CK(launch_bin_sort<float>(p->geom, Np, static_cast<const float*>(xd),
                                   static_cast<const float*>(yd), static_cast<const float*>(zd),
                                   p->count, p->offset, p->blocksum, p->bin_of, p->rank_of,
-                                  p->perm, static_cast<float*>(p->dx), static_cast<float*>(p->dy),
-                                  static_cast<float*>(p->dz), p->la, p->nbins, p->stream));
+                                  static_cast<PtRec<float>*>(p->rec), p->nbins, p->stream));
     p->Np = Np;
     return NUFFT_OK;
 }
@@ -600,11 +608,7 @@ int nufft_destroy(nufft_handle p) {
     dev_free(p, (void**)&p->blocksum, 0);
     dev_free(p, (void**)&p->bin_of, 0);
     dev_free(p, (void**)&p->rank_of, 0);
-    dev_free(p, (void**)&p->perm, 0);
-    dev_free(p, (void**)&p->la, 0);
-    dev_free(p, &p->dx, 0);
-    dev_free(p, &p->dy, 0);
-    dev_free(p, &p->dz, 0);
+    dev_free(p, &p->rec, 0);
     dev_free(p, &p->stage_in, 0);
     dev_free(p, &p->stage_out, 0);
     if (p->timing)

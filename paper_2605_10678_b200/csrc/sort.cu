@@ -12,10 +12,9 @@
 //   k2 scan      : exclusive prefix sum of count[] -> offset[] with warp
 //                  __shfl_up_sync scans, three phases (tile sums, scan of sums,
 //                  tile scans + carry-in).
-//   k3 scatter   : slot = offset[bin] + rank; perm[slot] = j (one 4-byte write).
-//   k4 records   : in slot order, gather x[perm], y[perm], z[perm] and write the
-//                  sorted stencil record (local base la, phase offsets d)
-//                  coalesced.
+//   k3 scatter   : slot = offset[bin] + rank; the sorted 32-byte stencil record
+//                  (phase offsets d, local base la, caller index) is written
+//                  to the slot as one full DRAM sector.
 #include "internal.cuh"
 
 namespace nufft {
@@ -172,25 +171,17 @@ __device__ __forceinline__ void local_stencil(double s, int c, int T, int w, int
     *d = ls - a;
 }
 
-__global__ void __launch_bounds__(kSortThreads) scatter_perm_kernel(
-    int64_t Np, const uint32_t* __restrict__ bin_of, const uint32_t* __restrict__ rank_of,
-    const uint32_t* __restrict__ offset, uint32_t* __restrict__ perm) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < Np;
-         i += (int64_t)gridDim.x * blockDim.x)
-        perm[offset[bin_of[i]] + rank_of[i]] = (uint32_t)i;
-}
-
-// Sorted records, written coalesced in slot order (the coordinates are gathered
-// through perm): random 8-byte READS instead of five random partial-sector
-// writes per point.
+// slot = offset[bin] + rank; the whole 32-byte record (one full DRAM sector,
+// two 16-byte stores) goes to the slot: the only random access of setpts.
 template <typename T>
-__global__ void __launch_bounds__(kSortThreads) records_kernel(
+__global__ void __launch_bounds__(kSortThreads) scatter_kernel(
     Geom g, int64_t Np, const T* __restrict__ x, const T* __restrict__ y,
-    const T* __restrict__ z, const uint32_t* __restrict__ perm, T* __restrict__ dx,
-    T* __restrict__ dy, T* __restrict__ dz, uint32_t* __restrict__ la) {
-    for (int64_t slot = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; slot < Np;
-         slot += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t i = perm[slot];
+    const T* __restrict__ z, const uint32_t* __restrict__ bin_of,
+    const uint32_t* __restrict__ rank_of, const uint32_t* __restrict__ offset,
+    PtRec<T>* __restrict__ rec) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < Np;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t slot = offset[bin_of[i]] + rank_of[i];
         const double sx = fold_rescale((double)x[i], g.L, g.scale[0], g.nf[0]);
         const double sy = fold_rescale((double)y[i], g.L, g.scale[1], g.nf[1]);
         const double sz = fold_rescale((double)z[i], g.L, g.scale[2], g.nf[2]) - (double)g.z_lo;
@@ -200,10 +191,13 @@ __global__ void __launch_bounds__(kSortThreads) records_kernel(
         local_stencil(sy, cell_of(sy, g.nf[1]), g.T[1], g.w, &lay, &ddy);
         local_stencil(sz, cell_of(sz + (double)g.z_lo, g.nf[2]) - (int)g.z_lo, g.T[2], g.w, &laz,
                       &ddz);
-        dx[slot] = (T)ddx;
-        dy[slot] = (T)ddy;
-        dz[slot] = (T)ddz;
-        la[slot] = (uint32_t)lax | ((uint32_t)lay << 8) | ((uint32_t)laz << 16);
+        PtRec<T> r;
+        r.d[0] = (T)ddx;
+        r.d[1] = (T)ddy;
+        r.d[2] = (T)ddz;
+        r.la = (uint32_t)lax | ((uint32_t)lay << 8) | ((uint32_t)laz << 16);
+        r.perm = (uint32_t)i;
+        rec[slot] = r;
     }
 }
 
@@ -221,8 +215,8 @@ size_t scan_blocksum_elems(int64_t nbins) { return (size_t)((nbins + kScanTile -
 template <typename T>
 cudaError_t launch_bin_sort(const Geom& g, int64_t Np, const T* x, const T* y, const T* z,
                             uint32_t* count, uint32_t* offset, uint32_t* blocksum,
-                            uint32_t* bin_of, uint32_t* rank_of, uint32_t* perm, T* dx, T* dy,
-                            T* dz, uint32_t* la, int64_t nbins, cudaStream_t s) {
+                            uint32_t* bin_of, uint32_t* rank_of, PtRec<T>* rec, int64_t nbins,
+                            cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(count, 0, sizeof(uint32_t) * (size_t)nbins, s);
     if (e != cudaSuccess) return e;
     if (Np > 0) {
@@ -234,21 +228,19 @@ cudaError_t launch_bin_sort(const Geom& g, int64_t Np, const T* x, const T* y, c
     scan_sums<<<1, kScanThreads, 0, s>>>(blocksum, ntiles);
     scan_tiles<<<(unsigned)ntiles, kScanThreads, 0, s>>>(count, nbins, blocksum, offset);
     if (Np > 0) {
-        scatter_perm_kernel<<<grid_for(Np, kSortThreads), kSortThreads, 0, s>>>(
-            Np, bin_of, rank_of, offset, perm);
-        records_kernel<T><<<grid_for(Np, kSortThreads), kSortThreads, 0, s>>>(
-            g, Np, x, y, z, perm, dx, dy, dz, la);
+        scatter_kernel<T><<<grid_for(Np, kSortThreads), kSortThreads, 0, s>>>(
+            g, Np, x, y, z, bin_of, rank_of, offset, rec);
     }
     return cudaGetLastError();
 }
 
 template cudaError_t launch_bin_sort<float>(const Geom&, int64_t, const float*, const float*,
                                             const float*, uint32_t*, uint32_t*, uint32_t*,
-                                            uint32_t*, uint32_t*, uint32_t*, float*, float*,
-                                            float*, uint32_t*, int64_t, cudaStream_t);
+                                            uint32_t*, uint32_t*, PtRec<float>*, int64_t,
+                                            cudaStream_t);
 template cudaError_t launch_bin_sort<double>(const Geom&, int64_t, const double*, const double*,
                                              const double*, uint32_t*, uint32_t*, uint32_t*,
-                                             uint32_t*, uint32_t*, uint32_t*, double*, double*,
-                                             double*, uint32_t*, int64_t, cudaStream_t);
+                                             uint32_t*, uint32_t*, PtRec<double>*, int64_t,
+                                             cudaStream_t);
 
 }  // namespace nufft

@@ -35,9 +35,8 @@ namespace {
 
 using namespace dev;
 
-// warps per CTA: plane owners (compile-time, so plane ownership is a mask, not a modulo)
-constexpr int kSpreadWarps = 4;
-constexpr int kSpreadThreads = 32 * kSpreadWarps;
+// NW = warps per CTA (4 or 8): the plane owners; compile-time, so plane ownership is
+// a mask, not a modulo.  Chosen per plan (opts spread_warps / built-in heuristic).
 // points staged per batch
 template <typename T> struct Batch;
 template <> struct Batch<float> { static constexpr int value = 64; };
@@ -57,15 +56,15 @@ struct SpreadSmem {
     static size_t bytes(int ncell) { return (size_t)ncell * sizeof(C) + batch_bytes(); }
 };
 
-template <typename T, int W>
-__global__ void __launch_bounds__(kSpreadThreads)
+template <typename T, int W, int NW>
+__global__ void __launch_bounds__(32 * NW)
     spread_tile_kernel(Geom g, PtsView<T> p, const typename Cx<T>::type* __restrict__ c,
                        typename Cx<T>::type* __restrict__ grid, T beta) {
     using C = typename Cx<T>::type;
     using S = SpreadSmem<T, W>;
     constexpr int B = S::B;
     constexpr int NQ = S::NQ;
-    constexpr int NW = kSpreadWarps;
+    constexpr int kSpreadThreads = 32 * NW;
     extern __shared__ __align__(16) unsigned char smem[];
 
     const int b = blockIdx.x;
@@ -100,20 +99,18 @@ __global__ void __launch_bounds__(kSpreadThreads)
     for (uint32_t p0 = beg; p0 < end; p0 += B) {
         const int n = (int)min((uint32_t)B, end - p0);
         __syncthreads();  // previous batch consumed (first round: tile zeroed)
-        // ---- phase A1: one thread per (point, axis): w ES weights; strength; base
-        for (int t = threadIdx.x; t < 3 * n; t += kSpreadThreads) {
+        // ---- phase A1: one thread per (point, axis, node): ES weight; strength; base
+        for (int e = threadIdx.x; e < 3 * W * n; e += kSpreadThreads) {
+            const int t = e / W, k = e - t * W;
             const int i = t / 3, d = t - 3 * i;
-            const uint32_t slot = p0 + i;
-            const T dd = d == 0 ? p.dx[slot] : (d == 1 ? p.dy[slot] : p.dz[slot]);
-            T* wd = sw1d + t * W;
-#pragma unroll
-            for (int k = 0; k < W; ++k) wd[k] = es_weight<T>(((T)k - dd) * two_over_w, beta);
-            if (d == 2) {
-                const uint32_t la = p.la[slot];
+            const PtRec<T>& rr = p.rec[p0 + i];
+            sw1d[e] = es_weight<T>(((T)k - rr.d[d]) * two_over_w, beta);
+            if (d == 2 && k == 0) {
+                const uint32_t la = rr.la;
                 const int lz = (int)(la >> 16);
                 sbase[i] = (lz * Ey + (int)((la >> 8) & 0xff)) * pitch + (int)(la & 0xff) + tx.shift;
                 slz[i] = lz;
-                scv[i] = c[p.perm[slot]];
+                scv[i] = c[rr.perm];
             }
         }
         __syncthreads();
@@ -182,20 +179,28 @@ size_t smem_w(const Geom& g) {
                                    (g.T[2] + W));
 }
 
-template <typename T, int W>
-cudaError_t launch_w(const Geom& g, const PtsView<T>& p, int64_t nbins,
+template <typename T, int W, int NW>
+cudaError_t launch_nw(const Geom& g, const PtsView<T>& p, int64_t nbins,
                      const typename Cx<T>::type* c, typename Cx<T>::type* grid, double beta,
                      cudaStream_t s) {
     const size_t smem = smem_w<T, W>(g);
-    auto kern = spread_tile_kernel<T, W>;
+    auto kern = spread_tile_kernel<T, W, NW>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return e;
     }
-    if (nbins > 0) kern<<<(unsigned)nbins, kSpreadThreads, smem, s>>>(g, p, c, grid, (T)beta);
+    if (nbins > 0) kern<<<(unsigned)nbins, 32 * NW, smem, s>>>(g, p, c, grid, (T)beta);
     return cudaGetLastError();
+}
+
+template <typename T, int W>
+cudaError_t launch_w(const Geom& g, const PtsView<T>& p, int64_t nbins,
+                     const typename Cx<T>::type* c, typename Cx<T>::type* grid, double beta,
+                     cudaStream_t s) {
+    return g.spread_warps == 8 ? launch_nw<T, W, 8>(g, p, nbins, c, grid, beta, s)
+                               : launch_nw<T, W, 4>(g, p, nbins, c, grid, beta, s);
 }
 
 }  // namespace

@@ -33,7 +33,7 @@ class Opts(ctypes.Structure):
     _fields_ = [("L", ctypes.c_double), ("modeord", ctypes.c_int), ("stream", ctypes.c_void_p),
                 ("comm", ctypes.c_void_p), ("points_owned", ctypes.c_int),
                 ("tile", ctypes.c_int * 3), ("timing", ctypes.c_int),
-                ("reserved", ctypes.c_int * 7)]
+                ("spread_warps", ctypes.c_int), ("reserved", ctypes.c_int * 6)]
 
 
 class Info(ctypes.Structure):
@@ -118,7 +118,7 @@ class Plan:
     """
 
     def __init__(self, N, eps, precision="f64", iflag=-1, L=2 * math.pi, modeord=0,
-                 device=None, stream=None, tile=None, timing=False):
+                 device=None, stream=None, tile=None, timing=False, spread_warps=0):
         if not torch.cuda.is_available():
             raise NufftError("libnufft requires a CUDA device (no CPU fallback)")
         self.N = tuple(int(n) for n in N)
@@ -135,6 +135,7 @@ class Plan:
         o.modeord = int(modeord)
         o.stream = self._stream.cuda_stream
         o.timing = 1 if timing else 0
+        o.spread_warps = int(spread_warps)
         if tile is not None:
             for d in range(3):
                 o.tile[d] = int(tile[d] if hasattr(tile, "__len__") else tile)

@@ -141,6 +141,24 @@ def test_nonuniform_shape_signs_modeord_landau(nb):
     assert np.allclose(np.fft.ifftshift(g1c), g1f, rtol=0, atol=1e-12 * np.abs(g1c).max())
 
 
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("kernel", [1, 4, 8])
+@pytest.mark.parametrize("eps", [1e-3, 1e-6, 1e-9])
+def test_every_spread_kernel(nb, prec, kernel, eps):
+    # 1 = register-row spread (T = 16 - w), 4 / 8 = shared-memory z-plane owners
+    if prec == "f32" and eps < 1e-7:
+        eps = 1e-7
+    w = nb.Plan((8, 8, 8), eps, precision=prec).info()["w"]
+    tile = 16 - w if kernel == 1 else 8
+    N, Np = (24, 24, 24), 20000
+    pts, c = host_inputs(Np, prec, seed=11)
+    fk = synthetic.modes(*N).to(c.dtype)
+    plan, g1, g2 = run_pair(nb, N, eps, prec, pts, c, fk, tile=tile, spread_warps=kernel)
+    x, y, z = (np64(p) for p in pts)
+    assert oracle.rel_l2(g1, oracle.type1(x, y, z, np64(c), N, eps)) <= TOL[prec]
+    assert oracle.rel_l2(g2, oracle.type2(x, y, z, np64(fk), eps)) <= TOL[prec]
+
+
 def test_custom_and_ragged_tiles(nb):
     N, Np, eps = (32, 32, 32), 30000, 1e-5
     pts, c = host_inputs(Np, "f64", seed=7)
