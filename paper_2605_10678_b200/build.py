@@ -28,7 +28,8 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler",
           "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 CU_FLAGS = ARCH + COMMON + ["--expt-relaxed-constexpr", "-Xptxas", "-v"]
 
-SOURCES = ["sort.cu", "spread.cu", "spread_rows.cu", "interp.cu", "elementwise.cu", "plan.cpp"]
+SOURCES = ["sort.cu", "spread.cu", "spread_rows.cu", "interp.cu", "elementwise.cu",
+           "dist_kernels.cu", "plan.cpp", "dist.cpp"]
 
 
 def _nccl_dirs():
@@ -61,6 +62,10 @@ def _compile(src, force, log):
     if not force and not _stale(obj, _deps(src)):
         return obj, ""
     flags = list(CU_FLAGS) if src.endswith(".cu") else ARCH + COMMON
+    inc, _ = _nccl_dirs()
+    if inc is None:
+        raise RuntimeError("nccl.h not found (expected torch's nvidia-nccl wheel)")
+    flags += ["-I", inc]
     cmd = [NVCC] + flags + ["-c", os.path.join(CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
@@ -84,8 +89,11 @@ def build(force: bool = False, jobs: int = 8, verbose: bool = False) -> str:
                 print(out)
     objs = [objs[s] for s in SOURCES]
     if force or _stale(LIB, objs):
+        _, ncl = _nccl_dirs()
+        # NCCL: torch's libnccl.so.2 (2.28), resolved through rpath at load time
         cmd = [NVCC] + ARCH + ["-shared", "-o", LIB + ".tmp"] + objs + \
-            ["-lcufft", "-Xlinker", "-rpath," + os.path.join(CUDA, "lib64")]
+            ["-lcufft", "-L", ncl, "-l:libnccl.so.2",
+             "-Xlinker", "-rpath," + os.path.join(CUDA, "lib64"), "-Xlinker", "-rpath," + ncl]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -1,0 +1,285 @@
+// dist_kernels.cu -- elementwise / packing kernels of the distributed (z-slab)
+// NUFFT (§2.4: "both grid values and particles
+// are partitioned according to the same spatial decomposition", halos of width
+// ceil(w/2), a distributed FFT).  All are one-pass, coalesced on their dense side.
+//
+//   owner_count   point -> owning rank (z-slab of its fine cell), rank within it
+//   pack / unpack move points, strengths and results to / from their owners
+//   halo_add      ghost planes received from a neighbour added to owned planes
+//   xy_pack       after the 2D (x, y) FFTs of the owned planes: keep the retained
+//                 x and y modes (chi is separable) and lay them out by the
+//                 destination rank of their y-mode block, ready for the all-to-all
+//   z_deconv      after the 1D z FFTs of this rank's y-block: keep the retained
+//                 z modes and apply D = p1 p2 p3
+//   z_pad         type-2 mirror: D then chi^T along z (zeros elsewhere)
+//   xy_unpad      type-2 mirror: received (x, y)-mode blocks -> zero-padded planes
+#include "internal.cuh"
+
+namespace nufft {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline unsigned grid1d(int64_t n) {
+    int64_t b = (n + kThreads - 1) / kThreads;
+    const int64_t cap = 148 * 32;
+    if (b > cap) b = cap;
+    return (unsigned)(b < 1 ? 1 : b);
+}
+
+__device__ __forceinline__ double fold_rescale_d(double x, double L, double scale, int64_t nf) {
+    double xf = x - L * floor(x / L);
+    double s = xf * scale;
+    if (s >= (double)nf) s -= (double)nf;
+    if (s < 0.0) s += (double)nf;
+    return s;
+}
+
+template <typename T>
+__global__ void owner_count_kernel(int64_t Np, const T* __restrict__ z, double L, double scale,
+                                   int64_t nf3, int nzl, uint32_t* __restrict__ owner,
+                                   uint32_t* __restrict__ rank_in, unsigned long long* counts) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i - lane < Np;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const bool live = i < Np;
+        uint32_t o = 0xffffffffu;
+        if (live) {
+            const double s = fold_rescale_d((double)z[i], L, scale, nf3);
+            int64_t c = (int64_t)s;
+            if (c >= nf3) c = nf3 - 1;
+            o = (uint32_t)(c / nzl);
+        }
+        const unsigned active = __ballot_sync(0xffffffffu, live);
+        if (live) {
+            const unsigned peers = __match_any_sync(active, o);
+            const int leader = __ffs(peers) - 1;
+            unsigned long long base = 0;
+            if (lane == leader) base = atomicAdd(&counts[o], (unsigned long long)__popc(peers));
+            base = __shfl_sync(peers, base, leader);
+            owner[i] = o;
+            rank_in[i] = (uint32_t)base + (uint32_t)__popc(peers & ((1u << lane) - 1u));
+        }
+    }
+}
+
+template <typename V>
+__global__ void pack_kernel(int64_t Np, const V* __restrict__ src, const uint32_t* __restrict__ owner,
+                            const uint32_t* __restrict__ rank_in,
+                            const unsigned long long* __restrict__ off, V* __restrict__ dst) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < Np;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[off[owner[i]] + rank_in[i]] = src[i];
+}
+
+template <typename V>
+__global__ void unpack_kernel(int64_t Np, const V* __restrict__ src,
+                              const uint32_t* __restrict__ owner,
+                              const uint32_t* __restrict__ rank_in,
+                              const unsigned long long* __restrict__ off, V* __restrict__ dst) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < Np;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[off[owner[i]] + rank_in[i]];
+}
+
+template <typename C>
+__global__ void halo_add_kernel(int64_t n, C* __restrict__ dst, const C* __restrict__ src) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        C a = dst[i];
+        const C b = src[i];
+        a.x += b.x;
+        a.y += b.y;
+        dst[i] = a;
+    }
+}
+
+__device__ __forceinline__ int64_t mode_of(int64_t i, int64_t N, int modeord) {
+    return modeord == 0 ? i - N / 2 : (i < N / 2 ? i : i - N);
+}
+
+// send[q][z][ys][x] = G[z][m2][m1], x in [0, N1), y storage index i2 = q*NY + ys
+template <typename C>
+__global__ void xy_pack_kernel(const C* __restrict__ G, int64_t nf1, int64_t nf2, int64_t nzl,
+                               int64_t N1, int64_t N2, int P, int modeord, C* __restrict__ send) {
+    const int64_t NY = N2 / P;
+    const int64_t total = nzl * N2 * N1;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i1 = t % N1;
+        const int64_t ys = (t / N1) % NY;
+        const int64_t z = (t / (N1 * NY)) % nzl;
+        const int64_t q = t / (N1 * NY * nzl);
+        const int64_t n1 = mode_of(i1, N1, modeord), n2 = mode_of(q * NY + ys, N2, modeord);
+        const int64_t m1 = n1 < 0 ? n1 + nf1 : n1, m2 = n2 < 0 ? n2 + nf2 : n2;
+        send[t] = G[(z * nf2 + m2) * nf1 + m1];
+    }
+}
+
+// fk[i3][ys][i1] = Z[m3][ys][i1] p1 p2 p3  (Z: nf3 lines of S = NY N1 values)
+template <typename T, typename C>
+__global__ void z_deconv_kernel(const C* __restrict__ Z, int64_t nf3, int64_t N1, int64_t NY,
+                                int64_t N2, int64_t N3, int64_t y0, const T* __restrict__ p1,
+                                const T* __restrict__ p2, const T* __restrict__ p3, int modeord,
+                                C* __restrict__ fk) {
+    const int64_t total = N3 * NY * N1;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i1 = t % N1, ys = (t / N1) % NY, i3 = t / (N1 * NY);
+        const int64_t n1 = mode_of(i1, N1, modeord), n2 = mode_of(y0 + ys, N2, modeord),
+                      n3 = mode_of(i3, N3, modeord);
+        const int64_t m3 = n3 < 0 ? n3 + nf3 : n3;
+        const T s = p1[n1 + N1 / 2] * p2[n2 + N2 / 2] * p3[n3 + N3 / 2];
+        const C v = Z[(m3 * NY + ys) * N1 + i1];
+        fk[t] = C{v.x * s, v.y * s};
+    }
+}
+
+// Z[m3][ys][i1] = fk[i3][ys][i1] p1 p2 p3 on retained m3, 0 elsewhere
+template <typename T, typename C>
+__global__ void z_pad_kernel(const C* __restrict__ fk, int64_t nf3, int64_t N1, int64_t NY,
+                             int64_t N2, int64_t N3, int64_t y0, const T* __restrict__ p1,
+                             const T* __restrict__ p2, const T* __restrict__ p3, int modeord,
+                             C* __restrict__ Z) {
+    const int64_t total = nf3 * NY * N1;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i1 = t % N1, ys = (t / N1) % NY, m3 = t / (N1 * NY);
+        C v{0, 0};
+        if (m3 < N3 / 2 || m3 >= nf3 - N3 / 2) {
+            const int64_t n3 = m3 < N3 / 2 ? m3 : m3 - nf3;
+            const int64_t i3 = modeord == 0 ? n3 + N3 / 2 : (n3 >= 0 ? n3 : n3 + N3);
+            const int64_t n1 = mode_of(i1, N1, modeord), n2 = mode_of(y0 + ys, N2, modeord);
+            const T s = p1[n1 + N1 / 2] * p2[n2 + N2 / 2] * p3[n3 + N3 / 2];
+            const C f = fk[(i3 * NY + ys) * N1 + i1];
+            v = C{f.x * s, f.y * s};
+        }
+        Z[t] = v;
+    }
+}
+
+// G[z][m2][m1] = recv[q][z][ys][i1] on retained (m1, m2), 0 elsewhere
+template <typename C>
+__global__ void xy_unpad_kernel(const C* __restrict__ recv, int64_t nf1, int64_t nf2,
+                                int64_t nzl, int64_t N1, int64_t N2, int P, int modeord,
+                                C* __restrict__ G) {
+    const int64_t NY = N2 / P;
+    const int64_t total = nzl * nf2 * nf1;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t m1 = t % nf1, m2 = (t / nf1) % nf2, z = t / (nf1 * nf2);
+        C v{0, 0};
+        const bool k1 = m1 < N1 / 2 || m1 >= nf1 - N1 / 2;
+        const bool k2 = m2 < N2 / 2 || m2 >= nf2 - N2 / 2;
+        if (k1 && k2) {
+            const int64_t n1 = m1 < N1 / 2 ? m1 : m1 - nf1, n2 = m2 < N2 / 2 ? m2 : m2 - nf2;
+            const int64_t i1 = modeord == 0 ? n1 + N1 / 2 : (n1 >= 0 ? n1 : n1 + N1);
+            const int64_t i2 = modeord == 0 ? n2 + N2 / 2 : (n2 >= 0 ? n2 : n2 + N2);
+            const int64_t q = i2 / NY, ys = i2 - q * NY;
+            v = recv[((q * nzl + z) * NY + ys) * N1 + i1];
+        }
+        G[t] = v;
+    }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- launchers
+template <typename T>
+cudaError_t launch_owner_count(int64_t Np, const T* z, double L, double scale, int64_t nf3,
+                               int nzl, uint32_t* owner, uint32_t* rank_in,
+                               unsigned long long* counts, cudaStream_t s) {
+    if (Np > 0)
+        owner_count_kernel<T><<<grid1d(Np), kThreads, 0, s>>>(Np, z, L, scale, nf3, nzl, owner,
+                                                              rank_in, counts);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack_bytes(int64_t Np, int elem_bytes, const void* src, const uint32_t* owner,
+                              const uint32_t* rank_in, const unsigned long long* off, void* dst,
+                              bool unpack, cudaStream_t s) {
+    if (Np <= 0) return cudaSuccess;
+    switch (elem_bytes) {
+        case 4:
+            if (unpack) unpack_kernel<float><<<grid1d(Np), kThreads, 0, s>>>(Np, (const float*)src, owner, rank_in, off, (float*)dst);
+            else pack_kernel<float><<<grid1d(Np), kThreads, 0, s>>>(Np, (const float*)src, owner, rank_in, off, (float*)dst);
+            break;
+        case 8:
+            if (unpack) unpack_kernel<double><<<grid1d(Np), kThreads, 0, s>>>(Np, (const double*)src, owner, rank_in, off, (double*)dst);
+            else pack_kernel<double><<<grid1d(Np), kThreads, 0, s>>>(Np, (const double*)src, owner, rank_in, off, (double*)dst);
+            break;
+        case 16:
+            if (unpack) unpack_kernel<double2><<<grid1d(Np), kThreads, 0, s>>>(Np, (const double2*)src, owner, rank_in, off, (double2*)dst);
+            else pack_kernel<double2><<<grid1d(Np), kThreads, 0, s>>>(Np, (const double2*)src, owner, rank_in, off, (double2*)dst);
+            break;
+        default:
+            return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_halo_add(int64_t n, typename Cx<T>::type* dst, const typename Cx<T>::type* src,
+                            cudaStream_t s) {
+    if (n > 0) halo_add_kernel<typename Cx<T>::type><<<grid1d(n), kThreads, 0, s>>>(n, dst, src);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_xy_pack(const typename Cx<T>::type* G, const int64_t nf[3], int64_t nzl,
+                           const int64_t N[3], int P, int modeord, typename Cx<T>::type* send,
+                           cudaStream_t s) {
+    xy_pack_kernel<typename Cx<T>::type><<<grid1d(nzl * N[1] * N[0]), kThreads, 0, s>>>(
+        G, nf[0], nf[1], nzl, N[0], N[1], P, modeord, send);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_z_deconv(const typename Cx<T>::type* Z, const int64_t nf[3], const int64_t N[3],
+                            int64_t NY, int64_t y0, const T* p1, const T* p2, const T* p3,
+                            int modeord, typename Cx<T>::type* fk, cudaStream_t s) {
+    z_deconv_kernel<T, typename Cx<T>::type><<<grid1d(N[2] * NY * N[0]), kThreads, 0, s>>>(
+        Z, nf[2], N[0], NY, N[1], N[2], y0, p1, p2, p3, modeord, fk);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_z_pad(const typename Cx<T>::type* fk, const int64_t nf[3], const int64_t N[3],
+                         int64_t NY, int64_t y0, const T* p1, const T* p2, const T* p3,
+                         int modeord, typename Cx<T>::type* Z, cudaStream_t s) {
+    z_pad_kernel<T, typename Cx<T>::type><<<grid1d(nf[2] * NY * N[0]), kThreads, 0, s>>>(
+        fk, nf[2], N[0], NY, N[1], N[2], y0, p1, p2, p3, modeord, Z);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_xy_unpad(const typename Cx<T>::type* recv, const int64_t nf[3], int64_t nzl,
+                            const int64_t N[3], int P, int modeord, typename Cx<T>::type* G,
+                            cudaStream_t s) {
+    xy_unpad_kernel<typename Cx<T>::type><<<grid1d(nzl * nf[1] * nf[0]), kThreads, 0, s>>>(
+        recv, nf[0], nf[1], nzl, N[0], N[1], P, modeord, G);
+    return cudaGetLastError();
+}
+
+#define NUFFT_DIST_INST(T)                                                                         \
+    template cudaError_t launch_owner_count<T>(int64_t, const T*, double, double, int64_t, int,      \
+                                               uint32_t*, uint32_t*, unsigned long long*,            \
+                                               cudaStream_t);                                        \
+    template cudaError_t launch_halo_add<T>(int64_t, Cx<T>::type*, const Cx<T>::type*,               \
+                                            cudaStream_t);                                           \
+    template cudaError_t launch_xy_pack<T>(const Cx<T>::type*, const int64_t*, int64_t,              \
+                                           const int64_t*, int, int, Cx<T>::type*, cudaStream_t);    \
+    template cudaError_t launch_z_deconv<T>(const Cx<T>::type*, const int64_t*, const int64_t*,      \
+                                            int64_t, int64_t, const T*, const T*, const T*, int,     \
+                                            Cx<T>::type*, cudaStream_t);                             \
+    template cudaError_t launch_z_pad<T>(const Cx<T>::type*, const int64_t*, const int64_t*,         \
+                                         int64_t, int64_t, const T*, const T*, const T*, int,        \
+                                         Cx<T>::type*, cudaStream_t);                                \
+    template cudaError_t launch_xy_unpad<T>(const Cx<T>::type*, const int64_t*, int64_t,             \
+                                            const int64_t*, int, int, Cx<T>::type*, cudaStream_t);
+NUFFT_DIST_INST(float)
+NUFFT_DIST_INST(double)
+#undef NUFFT_DIST_INST
+
+}  // namespace nufft

@@ -30,7 +30,23 @@ struct Geom {
     double scale[3];    // nf / L
     int w;              // kernel width
     int spread_warps;   // spread kernel: 1 = register rows, 4 / 8 = smem z-plane owners
+    // z boundary: 1 = periodic over nz_loc (one GPU); 0 = z-slab of a distributed
+    // plan, the grid pointer addresses local plane 0 and planes [-hz_lo, nz_loc + hz_hi)
+    // exist (ghost halos accumulated / filled over NCCL)
+    int zper;
+    int hz_lo, hz_hi;
 };
+
+// Local z row of a subgrid: periodic wrap on one GPU; on a slab, -1e9 marks a
+// row outside the halo-extended slab (never touched by any stencil).
+__host__ __device__ __forceinline__ int z_row(int gz, const Geom& g) {
+    if (g.zper) {
+        const int n = (int)g.nz_loc;
+        gz += gz < 0 ? n : 0;
+        return gz >= n ? gz - n : gz;
+    }
+    return (gz < -g.hz_lo || gz >= (int)g.nz_loc + g.hz_hi) ? -1000000000 : gz;
+}
 
 // Sorted point record written by setpts, one 32-byte (one DRAM sector) AoS
 // record per sorted slot:

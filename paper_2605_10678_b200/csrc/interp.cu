@@ -71,12 +71,16 @@ __global__ void __launch_bounds__(kInterpThreads, 2)
     __syncthreads();
     {
         const int oy = by * g.T[1] - W / 2, oz = bz * g.T[2] - W / 2;
-        const int nfx = (int)g.nf[0], nfy = (int)g.nf[1], nfz = (int)g.nz_loc;
+        const int nfx = (int)g.nf[0], nfy = (int)g.nf[1];
         int sg[2], ss[2], sn[2];
         const int nseg = row_segments(tx.gx0, pitch, nfx, sg, ss, sn);
         for (int r = threadIdx.x; r < Ey * Ez; r += kInterpThreads) {
             const int cz = r / Ey, cy = r - cz * Ey;
-            const int gy = wrap1(oy + cy, nfy), gz = wrap1(oz + cz, nfz);
+            int gz = z_row(oz + cz, g);
+            // a row beyond the halo-extended slab is read by no stencil: stage any
+            // valid row there (the transaction count stays one full subgrid)
+            if (gz < -g.hz_lo) gz = 0;
+            const int gy = wrap1(oy + cy, nfy);
             const C* grow = grid + (int64_t)nfx * ((int64_t)gz * nfy + gy);
             C* trow = tile + r * pitch;
             for (int k = 0; k < nseg; ++k)

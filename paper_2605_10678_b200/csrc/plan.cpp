@@ -4,19 +4,20 @@
 // Host-side orchestration only: parameter choice, the deconvolution table by
 // Gauss-Legendre quadrature (once per plan), device buffers,
 // the cuFFT plan, host<->device staging, CUDA-event stage timing.  Every step
-// of the NUFFT itself runs in the kernels of sort.cu / spread.cu / interp.cu /
-// elementwise.cu (and cuFFT for the uniform FFT).
+// of the NUFFT itself runs in the kernels of sort.cu / spread*.cu / interp.cu /
+// elementwise.cu (and cuFFT for the uniform FFT).  Plans with
+// opts.comm are z-slab plans whose execute path lives in dist.cpp.
 #include <cuda_runtime.h>
 #include <cufft.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
-#include <algorithm>
 #include <cstring>
 #include <new>
 #include <vector>
 
-#include "internal.cuh"
+#include "plan_state.h"
 
 using namespace nufft;
 
@@ -79,84 +80,6 @@ double es_phihat(double xi, double beta) {
     return h * acc;
 }
 
-}  // namespace nufft
-
-struct nufft_plan_s {
-    int prec = NUFFT_F64;
-    int iflag = -1;
-    double eps = 0;
-    int w = 0;
-    double beta = 0;
-    int modeord = 0;
-    int64_t N[3] = {0, 0, 0};
-    int64_t nf[3] = {0, 0, 0};
-    Geom geom{};
-    int64_t nbins = 0;
-    cudaStream_t stream = nullptr;
-    size_t real_size = 8;
-    size_t cplx_size = 16;
-
-    void* d_p[3] = {nullptr, nullptr, nullptr};  // deconvolution factors, precision type
-    void* d_grid = nullptr;                      // nf1 nf2 nf3 complex
-    size_t grid_bytes = 0;
-    cufftHandle fft = 0;
-    bool fft_ok = false;
-
-    // points
-    int64_t Np = -1;
-    int64_t cap = 0;
-    uint32_t* count = nullptr;
-    uint32_t* offset = nullptr;
-    uint32_t* blocksum = nullptr;
-    uint32_t* bin_of = nullptr;
-    uint32_t* rank_of = nullptr;
-    void* rec = nullptr;  // Np sorted 32-byte records (PtRec)
-
-    // host staging
-    void* stage_in = nullptr;
-    size_t stage_in_bytes = 0;
-    void* stage_out = nullptr;
-    size_t stage_out_bytes = 0;
-
-    // timing
-    bool timing = false;
-    cudaEvent_t ev0[8] = {};
-    cudaEvent_t ev[8] = {};
-    bool ev_used[8] = {};
-
-    size_t bytes = 0;
-};
-
-namespace {
-
-enum { EV_SETPTS = 0, EV_SPREAD, EV_FFT, EV_DECONV, EV_PAD, EV_INTERP };
-
-struct StageTimer {
-    nufft_plan_s* p;
-    int id;
-    StageTimer(nufft_plan_s* pl, int i) : p(pl), id(i) {
-        if (p->timing) cudaEventRecord(p->ev0[id], p->stream);
-    }
-    ~StageTimer() {
-        if (p->timing) {
-            cudaEventRecord(p->ev[id], p->stream);
-            p->ev_used[id] = true;
-        }
-    }
-};
-
-int cuda_status(cudaError_t e) {
-    if (e == cudaSuccess) return NUFFT_OK;
-    if (e == cudaErrorMemoryAllocation) return NUFFT_ERR_ALLOC;
-    return NUFFT_ERR_CUDA;
-}
-
-#define CK(expr)                                  \
-    do {                                          \
-        cudaError_t e__ = (expr);                 \
-        if (e__ != cudaSuccess) return cuda_status(e__); \
-    } while (0)
-
 bool is_device_ptr(const void* ptr) {
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
@@ -186,8 +109,6 @@ void dev_free(nufft_plan_s* p, void** ptr, size_t bytes) {
     }
 }
 
-// Device view of a caller array: device pointers pass through, host arrays are
-// copied into the plan's input staging buffer (offset `off` bytes into it).
 int input_view(nufft_plan_s* p, const void* src, size_t bytes, size_t off, size_t total,
                const void** dev) {
     if (bytes == 0 || is_device_ptr(src)) {
@@ -202,7 +123,7 @@ int input_view(nufft_plan_s* p, const void* src, size_t bytes, size_t off, size_
         p->stage_in_bytes = total;
     }
     char* d = static_cast<char*>(p->stage_in) + off;
-    CK(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, p->stream));
+    NUFFT_CK(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, p->stream));
     *dev = d;
     return NUFFT_OK;
 }
@@ -227,10 +148,91 @@ int output_view(nufft_plan_s* p, void* dst, size_t bytes, void** dev, bool* stag
 
 int finish_output(nufft_plan_s* p, void* dst, const void* dev, size_t bytes, bool staged) {
     if (!staged) return NUFFT_OK;
-    CK(cudaMemcpyAsync(dst, dev, bytes, cudaMemcpyDeviceToHost, p->stream));
-    CK(cudaStreamSynchronize(p->stream));
+    NUFFT_CK(cudaMemcpyAsync(dst, dev, bytes, cudaMemcpyDeviceToHost, p->stream));
+    NUFFT_CK(cudaStreamSynchronize(p->stream));
     return NUFFT_OK;
 }
+
+template <typename T>
+PtsView<T> pts_view(nufft_plan_s* p) {
+    PtsView<T> v;
+    v.offset = p->offset;
+    v.rec = static_cast<const PtRec<T>*>(p->rec);
+    return v;
+}
+
+int local_sort(nufft_plan_s* p, int64_t Np, const void* xd, const void* yd, const void* zd) {
+    if (Np >= (int64_t)1 << 31) return NUFFT_ERR_NPTS;
+    int st = NUFFT_OK;
+    if (Np > p->cap) {
+        dev_free(p, (void**)&p->bin_of, 4 * p->cap);
+        dev_free(p, (void**)&p->rank_of, 4 * p->cap);
+        dev_free(p, &p->rec, 32 * p->cap);
+        p->cap = 0;
+        const size_t n = (size_t)Np;
+        st = dev_alloc(p, (void**)&p->bin_of, 4 * n);
+        if (!st) st = dev_alloc(p, (void**)&p->rank_of, 4 * n);
+        if (!st) st = dev_alloc(p, &p->rec, 32 * n);
+        if (st) {
+            p->Np = -1;
+            return st;
+        }
+        p->cap = Np;
+    }
+    if (p->prec == NUFFT_F64)
+        NUFFT_CK(launch_bin_sort<double>(p->geom, Np, static_cast<const double*>(xd),
+                                         static_cast<const double*>(yd),
+                                         static_cast<const double*>(zd), p->count, p->offset,
+                                         p->blocksum, p->bin_of, p->rank_of,
+                                         static_cast<PtRec<double>*>(p->rec), p->nbins, p->stream));
+    else
+        NUFFT_CK(launch_bin_sort<float>(p->geom, Np, static_cast<const float*>(xd),
+                                        static_cast<const float*>(yd),
+                                        static_cast<const float*>(zd), p->count, p->offset,
+                                        p->blocksum, p->bin_of, p->rank_of,
+                                        static_cast<PtRec<float>*>(p->rec), p->nbins, p->stream));
+    p->Np = Np;
+    return NUFFT_OK;
+}
+
+int do_spread(nufft_plan_s* p, const void* c_dev, void* grid0) {
+    StageTimer tm(p, EV_SPREAD);
+    const bool rows = p->geom.spread_warps == 1;  // register-row kernel (plan checked it applies)
+    if (rows && p->prec == NUFFT_F64)
+        NUFFT_CK(launch_spread_rows<double>(p->geom, pts_view<double>(p), p->nbins,
+                                            static_cast<const double2*>(c_dev),
+                                            static_cast<double2*>(grid0), p->beta, p->stream));
+    else if (rows)
+        NUFFT_CK(launch_spread_rows<float>(p->geom, pts_view<float>(p), p->nbins,
+                                           static_cast<const float2*>(c_dev),
+                                           static_cast<float2*>(grid0), p->beta, p->stream));
+    else if (p->prec == NUFFT_F64)
+        NUFFT_CK(launch_spread<double>(p->geom, pts_view<double>(p), p->nbins,
+                                       static_cast<const double2*>(c_dev),
+                                       static_cast<double2*>(grid0), p->beta, p->stream));
+    else
+        NUFFT_CK(launch_spread<float>(p->geom, pts_view<float>(p), p->nbins,
+                                      static_cast<const float2*>(c_dev),
+                                      static_cast<float2*>(grid0), p->beta, p->stream));
+    return NUFFT_OK;
+}
+
+int do_interp(nufft_plan_s* p, const void* grid0, void* c_dev) {
+    StageTimer tm(p, EV_INTERP);
+    if (p->prec == NUFFT_F64)
+        NUFFT_CK(launch_interp<double>(p->geom, pts_view<double>(p), p->nbins,
+                                       static_cast<const double2*>(grid0),
+                                       static_cast<double2*>(c_dev), p->beta, p->stream));
+    else
+        NUFFT_CK(launch_interp<float>(p->geom, pts_view<float>(p), p->nbins,
+                                      static_cast<const float2*>(grid0),
+                                      static_cast<float2*>(c_dev), p->beta, p->stream));
+    return NUFFT_OK;
+}
+
+}  // namespace nufft
+
+namespace {
 
 // Default bin edge by width (measured on B200, profiles/README.md): fp32 uses the
 // register-row spread, whose subgrid is 16 x 16 x 16 cells (T = 16 - w); fp64 uses
@@ -242,50 +244,6 @@ int default_tile(int w, int prec, int64_t nf) {
     if (t > 64) t = 64;
     if (t > nf - w - 2) t = (int)(nf - w - 2);  // T + w + 2 <= nf: one-step periodic wraps, <= 2 row segments
     return t;
-}
-
-template <typename T>
-PtsView<T> pts_view(nufft_plan_s* p) {
-    PtsView<T> v;
-    v.offset = p->offset;
-    v.rec = static_cast<const PtRec<T>*>(p->rec);
-    return v;
-}
-
-int do_spread(nufft_plan_s* p, const void* c_dev, void* grid_dev) {
-    CK(cudaMemsetAsync(grid_dev, 0, p->grid_bytes, p->stream));
-    StageTimer tm(p, EV_SPREAD);
-    const bool rows = p->geom.spread_warps == 1;  // register-row kernel (plan checked it applies)
-    if (rows && p->prec == NUFFT_F64)
-        CK(launch_spread_rows<double>(p->geom, pts_view<double>(p), p->nbins,
-                                      static_cast<const double2*>(c_dev),
-                                      static_cast<double2*>(grid_dev), p->beta, p->stream));
-    else if (rows)
-        CK(launch_spread_rows<float>(p->geom, pts_view<float>(p), p->nbins,
-                                     static_cast<const float2*>(c_dev),
-                                     static_cast<float2*>(grid_dev), p->beta, p->stream));
-    else if (p->prec == NUFFT_F64)
-        CK(launch_spread<double>(p->geom, pts_view<double>(p), p->nbins,
-                                 static_cast<const double2*>(c_dev),
-                                 static_cast<double2*>(grid_dev), p->beta, p->stream));
-    else
-        CK(launch_spread<float>(p->geom, pts_view<float>(p), p->nbins,
-                                static_cast<const float2*>(c_dev), static_cast<float2*>(grid_dev),
-                                p->beta, p->stream));
-    return NUFFT_OK;
-}
-
-int do_interp(nufft_plan_s* p, const void* grid_dev, void* c_dev) {
-    StageTimer tm(p, EV_INTERP);
-    if (p->prec == NUFFT_F64)
-        CK(launch_interp<double>(p->geom, pts_view<double>(p), p->nbins,
-                                 static_cast<const double2*>(grid_dev),
-                                 static_cast<double2*>(c_dev), p->beta, p->stream));
-    else
-        CK(launch_interp<float>(p->geom, pts_view<float>(p), p->nbins,
-                                static_cast<const float2*>(grid_dev), static_cast<float2*>(c_dev),
-                                p->beta, p->stream));
-    return NUFFT_OK;
 }
 
 int do_fft(nufft_plan_s* p, int sign) {
@@ -300,6 +258,8 @@ int do_fft(nufft_plan_s* p, int sign) {
                          static_cast<cufftComplex*>(p->d_grid), dir);
     return r == CUFFT_SUCCESS ? NUFFT_OK : NUFFT_ERR_CUFFT;
 }
+
+int64_t user_np(nufft_plan_s* p) { return p->dist ? dist_user_np(p) : p->Np; }
 
 }  // namespace
 
@@ -317,7 +277,7 @@ const char* nufft_strerror(int code) {
         case NUFFT_OK: return "ok";
         case NUFFT_WARN_EPS_CLAMPED: return "warning: eps clamped to the supported range";
         case NUFFT_ERR_ARG: return "invalid argument";
-        case NUFFT_ERR_MODES: return "invalid mode counts (need even N >= 2 with 2N >= w)";
+        case NUFFT_ERR_MODES: return "invalid mode counts (need even N >= 2 with 2N >= w + 3)";
         case NUFFT_ERR_NPTS: return "invalid number of points";
         case NUFFT_ERR_NOT_SET: return "points not set (call nufft_setpts first)";
         case NUFFT_ERR_ALLOC: return "device allocation failed";
@@ -338,7 +298,8 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
     if (opts) o = *opts;
     else nufft_default_opts(&o);
     if (!(o.L > 0) || (o.modeord != 0 && o.modeord != 1)) return NUFFT_ERR_ARG;
-    if (o.comm) return NUFFT_ERR_UNSUPPORTED;
+    if (o.spread_warps != 0 && o.spread_warps != 1 && o.spread_warps != 4 && o.spread_warps != 8)
+        return NUFFT_ERR_ARG;
 
     nufft_plan_s* p = new (std::nothrow) nufft_plan_s();
     if (!p) return NUFFT_ERR_ALLOC;
@@ -359,6 +320,8 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
     p->real_size = precision == NUFFT_F64 ? 8 : 4;
     p->cplx_size = 2 * p->real_size;
     p->timing = o.timing != 0;
+    p->comm = o.comm;
+    p->points_owned = o.points_owned;
 
     Geom& g = p->geom;
     for (int d = 0; d < 3; ++d) {
@@ -376,14 +339,12 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
     g.w = p->w;
     g.z_lo = 0;
     g.nz_loc = p->nf[2];
+    g.zper = 1;
+    g.hz_lo = 0;
+    g.hz_hi = 0;
     // spread kernel: 1 = register rows (needs w <= 12 and T = 16 - w), 4 / 8 = shared-
     // memory z-plane owners with that many warps; 0 = rows for fp32 when they apply,
     // else 8 z-plane owners (the faster pair on B200 per precision, profiles/README.md)
-    if (o.spread_warps != 0 && o.spread_warps != 1 && o.spread_warps != 4 &&
-        o.spread_warps != 8) {
-        delete p;
-        return NUFFT_ERR_ARG;
-    }
     g.spread_warps = o.spread_warps;
     if (g.spread_warps == 0)
         g.spread_warps = (precision == NUFFT_F32 && spread_rows_applies(g)) ? 1 : 8;
@@ -391,7 +352,6 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
         delete p;
         return NUFFT_ERR_UNSUPPORTED;
     }
-    p->nbins = (int64_t)g.nb[0] * g.nb[1] * g.nb[2];
 
     // the (T + w)^3 subgrid (+ staging) of the spread / interp kernels must fit in
     // the opt-in shared memory of one CTA
@@ -433,23 +393,29 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
             st = cuda_status(cudaMemcpy(p->d_p[d], pf.data(), pf.size() * 4, cudaMemcpyHostToDevice));
         }
     }
-    p->grid_bytes = (size_t)(p->nf[0] * p->nf[1] * p->nf[2]) * p->cplx_size;
-    if (!st) st = dev_alloc(p, &p->d_grid, p->grid_bytes);
+    if (!st && p->comm) {
+        st = dist_init(p);  // z-slab geometry, halo grid, buffers, slab FFT plans
+    } else if (!st) {
+        p->nbins = (int64_t)g.nb[0] * g.nb[1] * g.nb[2];
+        p->grid_bytes = (size_t)(p->nf[0] * p->nf[1] * p->nf[2]) * p->cplx_size;
+        st = dev_alloc(p, &p->d_grid, p->grid_bytes);
+        p->grid0 = p->d_grid;
+        if (!st) {
+            cufftResult r = cufftPlan3d(&p->fft, (int)p->nf[2], (int)p->nf[1], (int)p->nf[0],
+                                        precision == NUFFT_F64 ? CUFFT_Z2Z : CUFFT_C2C);
+            if (r != CUFFT_SUCCESS) st = NUFFT_ERR_CUFFT;
+            else {
+                p->fft_ok = true;
+                size_t ws = 0;
+                cufftGetSize(p->fft, &ws);
+                p->bytes += ws;
+                if (cufftSetStream(p->fft, p->stream) != CUFFT_SUCCESS) st = NUFFT_ERR_CUFFT;
+            }
+        }
+    }
     if (!st) st = dev_alloc(p, (void**)&p->count, sizeof(uint32_t) * (size_t)p->nbins);
     if (!st) st = dev_alloc(p, (void**)&p->offset, sizeof(uint32_t) * (size_t)(p->nbins + 1));
     if (!st) st = dev_alloc(p, (void**)&p->blocksum, sizeof(uint32_t) * scan_blocksum_elems(p->nbins));
-    if (!st) {
-        cufftResult r = cufftPlan3d(&p->fft, (int)p->nf[2], (int)p->nf[1], (int)p->nf[0],
-                                    precision == NUFFT_F64 ? CUFFT_Z2Z : CUFFT_C2C);
-        if (r != CUFFT_SUCCESS) st = NUFFT_ERR_CUFFT;
-        else {
-            p->fft_ok = true;
-            size_t ws = 0;
-            cufftGetSize(p->fft, &ws);
-            p->bytes += ws;
-            if (cufftSetStream(p->fft, p->stream) != CUFFT_SUCCESS) st = NUFFT_ERR_CUFFT;
-        }
-    }
     if (!st && p->timing)
         for (int i = 0; i < 8; ++i) {
             cudaEventCreate(&p->ev0[i]);
@@ -470,44 +436,21 @@ int nufft_setpts(nufft_handle p, int64_t Np, const void* x, const void* y, const
     if (Np > 0 && (!x || !y || !z)) return NUFFT_ERR_ARG;
     StageTimer tm(p, EV_SETPTS);
     int st = NUFFT_OK;
-    if (Np > p->cap) {
-        dev_free(p, (void**)&p->bin_of, 4 * p->cap);
-        dev_free(p, (void**)&p->rank_of, 4 * p->cap);
-        dev_free(p, &p->rec, 32 * p->cap);
-        p->cap = 0;
-        const size_t n = (size_t)Np;
-        st = dev_alloc(p, (void**)&p->bin_of, 4 * n);
-        if (!st) st = dev_alloc(p, (void**)&p->rank_of, 4 * n);
-        if (!st) st = dev_alloc(p, &p->rec, 32 * n);
-        if (st) {
-            p->Np = -1;
-            return st;
-        }
-        p->cap = Np;
-    }
     const size_t b = (size_t)Np * p->real_size;
     const void *xd = nullptr, *yd = nullptr, *zd = nullptr;
     if ((st = input_view(p, x, b, 0, 3 * b, &xd))) return st;
     if ((st = input_view(p, y, b, b, 3 * b, &yd))) return st;
     if ((st = input_view(p, z, b, 2 * b, 3 * b, &zd))) return st;
-    if (p->prec == NUFFT_F64)
-        CK(launch_bin_sort<double>(p->geom, Np, static_cast<const double*>(xd),
-                                   static_cast<const double*>(yd), static_cast<const double*>(zd),
-                                   p->count, p->offset, p->blocksum, p->bin_of, p->rank_of,
-                                   static_cast<PtRec<double>*>(p->rec), p->nbins, p->stream));
-    else
-        CK(launch_bin_sort<float>(p->geom, Np, static_cast<const float*>(xd),
-                                  static_cast<const float*>(yd), static_cast<const float*>(zd),
-                                  p->count, p->offset, p->blocksum, p->bin_of, p->rank_of,
-                                  static_cast<PtRec<float>*>(p->rec), p->nbins, p->stream));
-    p->Np = Np;
-    return NUFFT_OK;
+    if (p->dist) return dist_setpts(p, Np, xd, yd, zd);
+    return local_sort(p, Np, xd, yd, zd);
 }
 
 int nufft_execute_type1(nufft_handle p, const void* c, void* fk) {
     cudaGetLastError();  // a stale non-sticky error of another caller is not ours
-    if (!p || !fk || (!c && p->Np > 0)) return NUFFT_ERR_ARG;
+    if (!p || !fk) return NUFFT_ERR_ARG;
     if (p->Np < 0) return NUFFT_ERR_NOT_SET;
+    if (!c && user_np(p) > 0) return NUFFT_ERR_ARG;
+    if (p->dist) return dist_type1(p, c, fk);
     int st;
     const void* cd = nullptr;
     if ((st = input_view(p, c, (size_t)p->Np * p->cplx_size, 0, (size_t)p->Np * p->cplx_size, &cd)))
@@ -516,18 +459,19 @@ int nufft_execute_type1(nufft_handle p, const void* c, void* fk) {
     void* fkd = nullptr;
     bool staged = false;
     if ((st = output_view(p, fk, fk_bytes, &fkd, &staged))) return st;
-    if ((st = do_spread(p, cd, p->d_grid))) return st;                 // Step 1: C
+    NUFFT_CK(cudaMemsetAsync(p->d_grid, 0, p->grid_bytes, p->stream));
+    if ((st = do_spread(p, cd, p->grid0))) return st;                   // Step 1: C
     if ((st = do_fft(p, p->iflag))) return st;                          // Step 2: F
     {
         StageTimer tm(p, EV_DECONV);                                    // Steps 3, 4: chi, D
         if (p->prec == NUFFT_F64)
-            CK(launch_truncate_deconv<double>(
+            NUFFT_CK(launch_truncate_deconv<double>(
                 static_cast<const double2*>(p->d_grid), p->nf, p->N,
                 static_cast<const double*>(p->d_p[0]), static_cast<const double*>(p->d_p[1]),
                 static_cast<const double*>(p->d_p[2]), p->modeord, static_cast<double2*>(fkd),
                 p->stream));
         else
-            CK(launch_truncate_deconv<float>(
+            NUFFT_CK(launch_truncate_deconv<float>(
                 static_cast<const float2*>(p->d_grid), p->nf, p->N,
                 static_cast<const float*>(p->d_p[0]), static_cast<const float*>(p->d_p[1]),
                 static_cast<const float*>(p->d_p[2]), p->modeord, static_cast<float2*>(fkd),
@@ -538,8 +482,10 @@ int nufft_execute_type1(nufft_handle p, const void* c, void* fk) {
 
 int nufft_execute_type2(nufft_handle p, const void* fk, void* c) {
     cudaGetLastError();  // a stale non-sticky error of another caller is not ours
-    if (!p || !fk || (!c && p->Np > 0)) return NUFFT_ERR_ARG;
+    if (!p || !fk) return NUFFT_ERR_ARG;
     if (p->Np < 0) return NUFFT_ERR_NOT_SET;
+    if (!c && user_np(p) > 0) return NUFFT_ERR_ARG;
+    if (p->dist) return dist_type2(p, fk, c);
     int st;
     const size_t fk_bytes = (size_t)(p->N[0] * p->N[1] * p->N[2]) * p->cplx_size;
     const void* fkd = nullptr;
@@ -551,24 +497,25 @@ int nufft_execute_type2(nufft_handle p, const void* fk, void* c) {
     {
         StageTimer tm(p, EV_PAD);                                       // D, chi^T
         if (p->prec == NUFFT_F64)
-            CK(launch_pad_precorrect<double>(
+            NUFFT_CK(launch_pad_precorrect<double>(
                 static_cast<const double2*>(fkd), p->N, static_cast<const double*>(p->d_p[0]),
                 static_cast<const double*>(p->d_p[1]), static_cast<const double*>(p->d_p[2]),
                 p->modeord, p->nf, static_cast<double2*>(p->d_grid), p->stream));
         else
-            CK(launch_pad_precorrect<float>(
+            NUFFT_CK(launch_pad_precorrect<float>(
                 static_cast<const float2*>(fkd), p->N, static_cast<const float*>(p->d_p[0]),
                 static_cast<const float*>(p->d_p[1]), static_cast<const float*>(p->d_p[2]),
                 p->modeord, p->nf, static_cast<float2*>(p->d_grid), p->stream));
     }
     if ((st = do_fft(p, -p->iflag))) return st;                         // F^-1
-    if ((st = do_interp(p, p->d_grid, cd))) return st;                  // C^T
+    if ((st = do_interp(p, p->grid0, cd))) return st;                   // C^T
     return finish_output(p, c, cd, c_bytes, staged);
 }
 
 int nufft_spread(nufft_handle p, const void* c, void* grid) {
     cudaGetLastError();  // a stale non-sticky error of another caller is not ours
     if (!p || !grid || (!c && p->Np > 0)) return NUFFT_ERR_ARG;
+    if (p->dist) return NUFFT_ERR_UNSUPPORTED;
     if (p->Np < 0) return NUFFT_ERR_NOT_SET;
     int st;
     const void* cd = nullptr;
@@ -577,6 +524,7 @@ int nufft_spread(nufft_handle p, const void* c, void* grid) {
     void* gd = nullptr;
     bool staged = false;
     if ((st = output_view(p, grid, p->grid_bytes, &gd, &staged))) return st;
+    NUFFT_CK(cudaMemsetAsync(gd, 0, p->grid_bytes, p->stream));
     if ((st = do_spread(p, cd, gd))) return st;
     return finish_output(p, grid, gd, p->grid_bytes, staged);
 }
@@ -584,6 +532,7 @@ int nufft_spread(nufft_handle p, const void* c, void* grid) {
 int nufft_interp(nufft_handle p, const void* grid, void* c) {
     cudaGetLastError();  // a stale non-sticky error of another caller is not ours
     if (!p || !grid || (!c && p->Np > 0)) return NUFFT_ERR_ARG;
+    if (p->dist) return NUFFT_ERR_UNSUPPORTED;
     if (p->Np < 0) return NUFFT_ERR_NOT_SET;
     int st;
     const void* gd = nullptr;
@@ -600,6 +549,7 @@ int nufft_destroy(nufft_handle p) {
     if (!p) return NUFFT_OK;
     if (p->stream) cudaStreamSynchronize(p->stream);
     else cudaDeviceSynchronize();
+    if (p->dist) dist_destroy(p);
     if (p->fft_ok) cufftDestroy(p->fft);
     for (int d = 0; d < 3; ++d) dev_free(p, &p->d_p[d], 0);
     dev_free(p, &p->d_grid, 0);
@@ -637,8 +587,14 @@ int nufft_get_info(nufft_handle p, nufft_info* info) {
     info->device_bytes = p->bytes;
     info->nranks = 1;
     info->rank = 0;
-    info->slab_lo = 0;
-    info->slab_hi = p->nf[2];
+    info->slab_lo = p->geom.z_lo;
+    info->slab_hi = p->geom.z_lo + p->geom.nz_loc;
+    if (p->dist) {
+        int64_t lo[3], hi[3];
+        dist_local_modes(p, lo, hi);
+        info->nranks = (int)(p->nf[2] / p->geom.nz_loc);
+        info->rank = (int)(p->geom.z_lo / p->geom.nz_loc);
+    }
     float ms[8];
     for (int i = 0; i < 8; ++i) {
         ms[i] = -1.0f;
@@ -652,24 +608,13 @@ int nufft_get_info(nufft_handle p, nufft_info* info) {
     info->ms_deconv = ms[EV_DECONV];
     info->ms_pad = ms[EV_PAD];
     info->ms_interp = ms[EV_INTERP];
-    info->ms_comm = -1;
+    info->ms_comm = ms[EV_COMM];
     return NUFFT_OK;
 }
 
-int nufft_comm_unique_id(char id[128]) {
-    (void)id;
-    return NUFFT_ERR_UNSUPPORTED;
-}
-int nufft_comm_init(const char id[128], int nranks, int rank, void** comm) {
-    (void)id, (void)nranks, (void)rank, (void)comm;
-    return NUFFT_ERR_UNSUPPORTED;
-}
-int nufft_comm_destroy(void* comm) {
-    (void)comm;
-    return NUFFT_ERR_UNSUPPORTED;
-}
 int nufft_local_modes(nufft_handle p, int64_t lo[3], int64_t hi[3]) {
     if (!p || !lo || !hi) return NUFFT_ERR_ARG;
+    if (p->dist) return dist_local_modes(p, lo, hi);
     for (int d = 0; d < 3; ++d) {
         lo[d] = 0;
         hi[d] = p->N[d];

@@ -1,0 +1,153 @@
+// plan_state.h -- the plan object behind `nufft_handle` and the host helpers
+// shared by plan.cpp (single GPU + ABI) and dist.cpp (z-slab decomposition).
+// Private to libnufft.so.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace nufft {
+struct DistState;  // dist.cpp
+}
+
+struct nufft_plan_s {
+    int prec = NUFFT_F64;
+    int iflag = -1;
+    double eps = 0;
+    int w = 0;
+    double beta = 0;
+    int modeord = 0;
+    int64_t N[3] = {0, 0, 0};
+    int64_t nf[3] = {0, 0, 0};
+    nufft::Geom geom{};
+    int64_t nbins = 0;
+    cudaStream_t stream = nullptr;
+    size_t real_size = 8;
+    size_t cplx_size = 16;
+
+    void* d_p[3] = {nullptr, nullptr, nullptr};  // deconvolution factors, precision type
+    void* d_grid = nullptr;   // fine grid (one GPU: nf1 nf2 nf3; slab: nf1 nf2 (hz_lo + nzl + hz_hi))
+    size_t grid_bytes = 0;    // bytes of d_grid
+    void* grid0 = nullptr;    // local plane 0 of the grid (== d_grid on one GPU)
+    cufftHandle fft = 0;      // one GPU: 3D plan
+    bool fft_ok = false;
+
+    // points (this rank's, after redistribution)
+    int64_t Np = -1;
+    int64_t cap = 0;
+    uint32_t* count = nullptr;
+    uint32_t* offset = nullptr;
+    uint32_t* blocksum = nullptr;
+    uint32_t* bin_of = nullptr;
+    uint32_t* rank_of = nullptr;
+    void* rec = nullptr;  // Np sorted 32-byte records (PtRec)
+
+    // host staging
+    void* stage_in = nullptr;
+    size_t stage_in_bytes = 0;
+    void* stage_out = nullptr;
+    size_t stage_out_bytes = 0;
+
+    // timing
+    bool timing = false;
+    cudaEvent_t ev0[8] = {};
+    cudaEvent_t ev[8] = {};
+    bool ev_used[8] = {};
+
+    // distributed (opts.comm != NULL)
+    void* comm = nullptr;                 // NufftComm*
+    nufft::DistState* dist = nullptr;
+    int points_owned = 0;
+
+    size_t bytes = 0;
+};
+
+namespace nufft {
+
+enum { EV_SETPTS = 0, EV_SPREAD, EV_FFT, EV_DECONV, EV_PAD, EV_INTERP, EV_COMM, EV_COUNT };
+
+struct StageTimer {
+    nufft_plan_s* p;
+    int id;
+    StageTimer(nufft_plan_s* pl, int i) : p(pl), id(i) {
+        if (p->timing) cudaEventRecord(p->ev0[id], p->stream);
+    }
+    ~StageTimer() {
+        if (p->timing) {
+            cudaEventRecord(p->ev[id], p->stream);
+            p->ev_used[id] = true;
+        }
+    }
+};
+
+inline int cuda_status(cudaError_t e) {
+    if (e == cudaSuccess) return NUFFT_OK;
+    if (e == cudaErrorMemoryAllocation) return NUFFT_ERR_ALLOC;
+    return NUFFT_ERR_CUDA;
+}
+
+#define NUFFT_CK(expr)                                        \
+    do {                                                      \
+        cudaError_t e__ = (expr);                             \
+        if (e__ != cudaSuccess) return nufft::cuda_status(e__); \
+    } while (0)
+
+bool is_device_ptr(const void* ptr);
+int dev_alloc(nufft_plan_s* p, void** ptr, size_t bytes);
+void dev_free(nufft_plan_s* p, void** ptr, size_t bytes);
+// device view of a caller input (host arrays staged into the input buffer at `off`)
+int input_view(nufft_plan_s* p, const void* src, size_t bytes, size_t off, size_t total,
+               const void** dev);
+// device view of a caller output (host arrays staged; finish_output copies back + syncs)
+int output_view(nufft_plan_s* p, void* dst, size_t bytes, void** dev, bool* staged);
+int finish_output(nufft_plan_s* p, void* dst, const void* dev, size_t bytes, bool staged);
+
+// counting sort of this rank's points (device arrays) into p->rec
+int local_sort(nufft_plan_s* p, int64_t Np, const void* x, const void* y, const void* z);
+// C: grid0 += C c (grid must be zeroed by the caller); C^T: c = C^T grid0
+int do_spread(nufft_plan_s* p, const void* c_dev, void* grid0);
+int do_interp(nufft_plan_s* p, const void* grid0, void* c_dev);
+
+// dist.cpp: the z-slab plan
+int dist_init(nufft_plan_s* p);
+int dist_setpts(nufft_plan_s* p, int64_t Np, const void* x, const void* y, const void* z);
+int dist_type1(nufft_plan_s* p, const void* c, void* fk);
+int dist_type2(nufft_plan_s* p, const void* fk, void* c);
+void dist_destroy(nufft_plan_s* p);
+int dist_local_modes(nufft_plan_s* p, int64_t lo[3], int64_t hi[3]);
+int64_t dist_user_np(nufft_plan_s* p);  // points the caller passed (before redistribution)
+
+// dist_kernels.cu launchers
+template <typename T>
+cudaError_t launch_owner_count(int64_t Np, const T* z, double L, double scale, int64_t nf3,
+                               int nzl, uint32_t* owner, uint32_t* rank_in,
+                               unsigned long long* counts, cudaStream_t s);
+cudaError_t launch_pack_bytes(int64_t Np, int elem_bytes, const void* src, const uint32_t* owner,
+                              const uint32_t* rank_in, const unsigned long long* off, void* dst,
+                              bool unpack, cudaStream_t s);
+template <typename T>
+cudaError_t launch_halo_add(int64_t n, typename Cx<T>::type* dst, const typename Cx<T>::type* src,
+                            cudaStream_t s);
+template <typename T>
+cudaError_t launch_xy_pack(const typename Cx<T>::type* G, const int64_t nf[3], int64_t nzl,
+                           const int64_t N[3], int P, int modeord, typename Cx<T>::type* send,
+                           cudaStream_t s);
+template <typename T>
+cudaError_t launch_z_deconv(const typename Cx<T>::type* Z, const int64_t nf[3], const int64_t N[3],
+                            int64_t NY, int64_t y0, const T* p1, const T* p2, const T* p3,
+                            int modeord, typename Cx<T>::type* fk, cudaStream_t s);
+template <typename T>
+cudaError_t launch_z_pad(const typename Cx<T>::type* fk, const int64_t nf[3], const int64_t N[3],
+                         int64_t NY, int64_t y0, const T* p1, const T* p2, const T* p3,
+                         int modeord, typename Cx<T>::type* Z, cudaStream_t s);
+template <typename T>
+cudaError_t launch_xy_unpad(const typename Cx<T>::type* recv, const int64_t nf[3], int64_t nzl,
+                            const int64_t N[3], int P, int modeord, typename Cx<T>::type* G,
+                            cudaStream_t s);
+
+}  // namespace nufft

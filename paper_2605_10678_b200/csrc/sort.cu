@@ -55,6 +55,9 @@ __global__ void __launch_bounds__(kSortThreads) bin_count_kernel(
             int cy = cell_of(fold_rescale((double)y[i], g.L, g.scale[1], g.nf[1]), g.nf[1]);
             int cz = cell_of(fold_rescale((double)z[i], g.L, g.scale[2], g.nf[2]), g.nf[2]) -
                      (int)g.z_lo;
+            // a slab plan given a point outside its slab (points_owned misuse): keep
+            // memory safe by clamping to the slab (the caller's contract is broken)
+            cz = cz < 0 ? 0 : (cz >= (int)g.nz_loc ? (int)g.nz_loc - 1 : cz);
             bin = (uint32_t)(cx / g.T[0]) +
                   (uint32_t)g.nb[0] * ((uint32_t)(cy / g.T[1]) + (uint32_t)g.nb[1] * (uint32_t)(cz / g.T[2]));
         }
@@ -184,7 +187,9 @@ __global__ void __launch_bounds__(kSortThreads) scatter_kernel(
         const uint32_t slot = offset[bin_of[i]] + rank_of[i];
         const double sx = fold_rescale((double)x[i], g.L, g.scale[0], g.nf[0]);
         const double sy = fold_rescale((double)y[i], g.L, g.scale[1], g.nf[1]);
-        const double sz = fold_rescale((double)z[i], g.L, g.scale[2], g.nf[2]) - (double)g.z_lo;
+        double sz = fold_rescale((double)z[i], g.L, g.scale[2], g.nf[2]) - (double)g.z_lo;
+        if (!(sz >= 0.0)) sz = 0.0;  // outside the slab: clamp (see bin_count_kernel)
+        if (sz >= (double)g.nz_loc) sz = (double)g.nz_loc - 0.5;
         int lax, lay, laz;
         double ddx, ddy, ddz;
         local_stencil(sx, cell_of(sx, g.nf[0]), g.T[0], g.w, &lax, &ddx);

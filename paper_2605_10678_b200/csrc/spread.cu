@@ -156,12 +156,13 @@ __global__ void __launch_bounds__(32 * NW)
     __syncthreads();
     // ---- flush: every subgrid row -> periodic fine grid, bulk reductions (UBLKRED)
     const int oy = by * g.T[1] - W / 2, oz = bz * g.T[2] - W / 2;
-    const int nfx = (int)g.nf[0], nfy = (int)g.nf[1], nfz = (int)g.nz_loc;
+    const int nfx = (int)g.nf[0], nfy = (int)g.nf[1];
     int sg[2], ss[2], sn[2];
     const int nseg = row_segments(tx.gx0, pitch, nfx, sg, ss, sn);
     for (int r = threadIdx.x; r < Ey * Ez; r += kSpreadThreads) {
         const int cz = r / Ey, cy = r - cz * Ey;
-        const int gy = wrap1(oy + cy, nfy), gz = wrap1(oz + cz, nfz);
+        const int gy = wrap1(oy + cy, nfy), gz = z_row(oz + cz, g);
+        if (gz < -g.hz_lo) continue;  // outside the halo-extended slab: all zero
         C* grow = grid + (int64_t)nfx * ((int64_t)gz * nfy + gy);
         const C* trow = tile + r * pitch;
         for (int k = 0; k < nseg; ++k)

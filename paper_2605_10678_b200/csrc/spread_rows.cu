@@ -156,16 +156,16 @@ __global__ void __launch_bounds__(kRowsThreads, 2)
     fence_proxy_async_smem();
     __syncthreads();
     const int oy = by * TT - W / 2, oz = bz * TT - W / 2;
-    const int nfx = (int)g.nf[0], nfy = (int)g.nf[1], nfz = (int)g.nz_loc;
+    const int nfx = (int)g.nf[0], nfy = (int)g.nf[1];
     int sg[2], ss[2], sn[2];
     const int nseg = row_segments(tx.gx0, P, nfx, sg, ss, sn);
     {
         const int r = threadIdx.x;  // one row per thread (E*E == kRowsThreads)
         const int cz = r / E, cy = r - cz * E;
-        const int gy = wrap1(oy + cy, nfy), gz = wrap1(oz + cz, nfz);
+        const int gy = wrap1(oy + cy, nfy), gz = z_row(oz + cz, g);
         C* grow = grid + (int64_t)nfx * ((int64_t)gz * nfy + gy);
         const C* trow = tile + r * P;
-        for (int k = 0; k < nseg; ++k)
+        for (int k = 0; k < (gz < -g.hz_lo ? 0 : nseg); ++k)
             bulk_red_add(reinterpret_cast<T*>(grow + sg[k]), trow + ss[k],
                          (unsigned)(sn[k] * sizeof(C)));
     }

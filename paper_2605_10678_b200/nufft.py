@@ -107,6 +107,33 @@ def _ptr(t: torch.Tensor, dtype, n: int, name: str) -> int:
     return t.data_ptr()
 
 
+class Comm:
+    """libnufft's NCCL communicator for a z-slab plan (one process per GPU).
+
+    The 128-byte NCCL id made by rank 0 (nufft_comm_unique_id) travels through the
+    torch.distributed process group; every rank then calls nufft_comm_init.
+    """
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.rank = dist.get_rank(group)
+        self.size = dist.get_world_size(group)
+        uid = ctypes.create_string_buffer(128)
+        if self.rank == 0:
+            _check(lib().nufft_comm_unique_id(uid), "nufft_comm_unique_id")
+        box = [uid.raw if self.rank == 0 else None]
+        dist.broadcast_object_list(box, src=0, group=group)
+        uid = ctypes.create_string_buffer(box[0], 128)
+        h = ctypes.c_void_p()
+        _check(lib().nufft_comm_init(uid, self.size, self.rank, ctypes.byref(h)), "nufft_comm_init")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().nufft_comm_destroy(self._h)
+            self._h = None
+
+
 class Plan:
     """One NUFFT plan (type 1 and type 2 share the points and the fine grid).
 
@@ -115,10 +142,13 @@ class Plan:
     precision: "f32" | "f64"
     iflag    : sign of the type-1 exponent (-1 = PAPER.md Eq. 1); type 2 uses -iflag
     L        : period of the point domain [0, L)^3
+    comm     : a Comm -> z-slab plan over its ranks (modes are y-slabs: local_modes())
+    points_owned : distributed only; 1 = every point given lies in this rank's z-slab
     """
 
     def __init__(self, N, eps, precision="f64", iflag=-1, L=2 * math.pi, modeord=0,
-                 device=None, stream=None, tile=None, timing=False, spread_warps=0):
+                 device=None, stream=None, tile=None, timing=False, spread_warps=0,
+                 comm=None, points_owned=False):
         if not torch.cuda.is_available():
             raise NufftError("libnufft requires a CUDA device (no CPU fallback)")
         self.N = tuple(int(n) for n in N)
@@ -136,6 +166,10 @@ class Plan:
         o.stream = self._stream.cuda_stream
         o.timing = 1 if timing else 0
         o.spread_warps = int(spread_warps)
+        if comm is not None:
+            o.comm = comm._h
+            o.points_owned = 1 if points_owned else 0
+        self.comm = comm
         if tile is not None:
             for d in range(3):
                 o.tile[d] = int(tile[d] if hasattr(tile, "__len__") else tile)
@@ -147,6 +181,16 @@ class Plan:
         self.status = st
         self._h = h
         self.Np = None
+        lo = (ctypes.c_int64 * 3)()
+        hi = (ctypes.c_int64 * 3)()
+        _check(lib().nufft_local_modes(h, lo, hi), "nufft_local_modes")
+        self.modes_lo, self.modes_hi = tuple(lo), tuple(hi)
+        # this rank's mode block, (z, y, x) storage order, x fastest
+        self.local_shape = tuple(hi[d] - lo[d] for d in (2, 1, 0))
+
+    def local_modes(self):
+        """[lo, hi) storage-index ranges per axis (x, y, z) of this rank's modes."""
+        return self.modes_lo, self.modes_hi
 
     # -- lifecycle
     def close(self):
@@ -190,18 +234,16 @@ class Plan:
                            pin_memory=(dev.type == "cpu" and torch.cuda.is_available()))
 
     def type1(self, c: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
-        N1, N2, N3 = self.N
-        fk = self._out(out, (N3, N2, N1), c)
+        fk = self._out(out, self.local_shape, c)
         pc = _ptr(c, self.cplx, self.Np, "c")
-        pf = _ptr(fk, self.cplx, N1 * N2 * N3, "fk")
+        pf = _ptr(fk, self.cplx, math.prod(self.local_shape), "fk")
         with torch.cuda.device(self.device):
             _check(lib().nufft_execute_type1(self._h, pc, pf), "nufft_execute_type1")
         return fk
 
     def type2(self, fk: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
-        N1, N2, N3 = self.N
         c = self._out(out, (self.Np,), fk)
-        pf = _ptr(fk, self.cplx, N1 * N2 * N3, "fk")
+        pf = _ptr(fk, self.cplx, math.prod(self.local_shape), "fk")
         pc = _ptr(c, self.cplx, self.Np, "c")
         with torch.cuda.device(self.device):
             _check(lib().nufft_execute_type2(self._h, pf, pc), "nufft_execute_type2")
