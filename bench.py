@@ -12,9 +12,11 @@ timed events.  `e2e` is the same metric through the C ABI with pinned HOST
 buffers (H2D of x, y, z, c, fk and D2H of fk, c inside the timed region).
 
 Default workload = BASELINE.json configs[1] (C2b: fp32, 128^3 modes, 2^21
-uniform points, eps = 1e-6).  N > 1 (torchrun): every rank runs an independent
-replica of the workload with its own seed ("scaling": "weak", no data-path
-collective); the distributed slab path is reported separately once built.
+uniform points, eps = 1e-6).  N > 1 (torchrun): the SAME workload on a z-slab
+plan over NCCL ("scaling": "strong"): each rank starts with Np/N points drawn
+over the whole domain (setpts redistributes them to their slab owners), halos
+are exchanged with the z-neighbours and the slab FFT transposes with
+ncclAlltoAll; value = all points / max-over-ranks device time per step.
 
 --impl reference: the CPU oracle (oracle/, plain C++ fp64) on the same config,
 rank 0 only, each step a bounded sample of the workload (2^19 points).
@@ -123,18 +125,24 @@ def dist_env():
     return ws, rank, local
 
 
-def make_inputs(cfg, rank, device):
+def make_inputs(cfg, rank, ws, device, mode_block=None):
+    """This rank's share of the workload: Np / ws points drawn uniformly (or Landau)
+    over the WHOLE domain with a rank-shifted seed -- so most start on the wrong
+    slab and setpts redistributes them -- and its block of the global modes."""
     import synthetic
     rdt = torch.float64 if cfg["prec"] == "f64" else torch.float32
     cdt = torch.complex128 if cfg["prec"] == "f64" else torch.complex64
-    Np = cfg["Np"]
+    Np = cfg["Np"] // ws + (1 if rank < cfg["Np"] % ws else 0)
     seed_shift = 1000 * rank
     if cfg["kind"] == "landau":
         pts = synthetic.landau_points(Np, seed=1 + seed_shift, device=device, dtype=rdt)
     else:
         pts = synthetic.uniform_points(Np, seed=1 + seed_shift, device=device, dtype=rdt)
     c = synthetic.strengths(Np, seed=2 + seed_shift, device=device, dtype=cdt)
-    fk = synthetic.modes(*cfg["N"], seed=3 + seed_shift, device=device, dtype=cdt)
+    fk = synthetic.modes(*cfg["N"], seed=3, device=device, dtype=cdt)
+    if mode_block is not None:
+        lo, hi = mode_block
+        fk = fk[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]].contiguous()
     return pts, c, fk
 
 
@@ -168,10 +176,12 @@ def run_ours(args, cfg):
     torch.cuda.set_device(device)
     stream = torch.cuda.current_stream(device)
 
-    pts, c, fk = make_inputs(cfg, rank, device)
-    N, Np = cfg["N"], cfg["Np"]
+    N, Np_total = cfg["N"], cfg["Np"]
+    comm = nb.Comm() if ws > 1 else None   # z-slab plan over NCCL
     plan = nb.Plan(N, cfg["eps"], precision=cfg["prec"], timing=True, device=device,
-                   tile=args.tile, spread_warps=args.spread_warps)
+                   tile=args.tile, spread_warps=args.spread_warps, comm=comm)
+    pts, c, fk = make_inputs(cfg, rank, ws, device, plan.local_modes() if ws > 1 else None)
+    Np = pts[0].numel()
     c2 = torch.empty(Np, dtype=c.dtype, device=device)
     fk_out = torch.empty_like(fk)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=device)
@@ -188,7 +198,7 @@ def run_ours(args, cfg):
     sampler = ClockSampler(local)
     sampler.start()
     stage = {k: [] for k in ("ms_setpts", "ms_spread", "ms_fft", "ms_deconv", "ms_pad",
-                             "ms_interp")}
+                             "ms_interp", "ms_comm")}
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
     if ws > 1:
@@ -213,7 +223,7 @@ def run_ours(args, cfg):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         t_max = float(t.item())
     ms_per_step = t_max / args.steps
-    value = ws * Np / (ms_per_step / 1e3)
+    value = Np_total / (ms_per_step / 1e3)   # all ranks' points per second
 
     # -- end to end through the C ABI with pinned host buffers
     hp = [p.cpu().pin_memory() for p in pts]
@@ -245,16 +255,20 @@ def run_ours(args, cfg):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         te = float(t.item())
     r = 8 if cfg["prec"] == "f64" else 4
-    nmodes = N[0] * N[1] * N[2]
+    nmodes = fk.numel()  # this rank's mode block
     h2d = 3 * Np * r + Np * 2 * r + nmodes * 2 * r
     d2h = nmodes * 2 * r + Np * 2 * r
+    if ws > 1:  # whole-job bytes
+        tot = torch.tensor([h2d, d2h], device=device, dtype=torch.float64)
+        torch.distributed.all_reduce(tot)
+        h2d, d2h = int(tot[0].item()), int(tot[1].item())
 
     # -- roofline of the dominant kernel of ours (spread or interp)
     med = {k: statistics.median(v) for k, v in stage.items() if v and min(v) >= 0}
     dom = "spread" if med.get("ms_spread", 0) >= med.get("ms_interp", 0) else "interp"
     dom_ms = med["ms_" + dom]
     hbm, peak_src = peaks()
-    bytes_alg = algorithmic_bytes(cfg, dom)
+    bytes_alg = algorithmic_bytes(cfg, dom) / ws   # this rank's share of the launch
     achieved = bytes_alg / (dom_ms / 1e3) / 1e9
     out = None
     if rank == 0:
@@ -263,17 +277,17 @@ def run_ours(args, cfg):
             "metric": "NUFFT points/s (setpts + type-1 spread + type-2 interp per point)",
             "value": value, "unit": "points/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None,
+            "scaling": "strong", "vs_baseline": None,
             "dtype": "f64" if cfg["prec"] == "f64" else "f32", "data": "synthetic",
             "config": {"workload": f"{cfg['name']}: {cfg['prec']} {N[0]}x{N[1]}x{N[2]} modes, "
-                                   f"{Np} {cfg['kind']} points, eps={cfg['eps']:g}",
-                       "N": list(N), "Np_per_gpu": Np, "eps": cfg["eps"], "w": plan.info()["w"],
-                       "precision": cfg["prec"], "points": cfg["kind"],
+                                   f"{Np_total} {cfg['kind']} points, eps={cfg['eps']:g}",
+                       "N": list(N), "Np_total": Np_total, "eps": cfg["eps"],
+                       "w": plan.info()["w"], "precision": cfg["prec"], "points": cfg["kind"],
                        "tile": plan.info()["tile"],
-                       "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU",
+                       "parallelism": f"z-slab x{ws} (NCCL halos + all-to-all)" if ws > 1 else "1 GPU",
                        "l2": "flushed (512 MB write) before every timed step"},
             "stage_ms_median": med,
-            "e2e": {"value": ws * Np / (te / e2e_steps / 1e3), "unit": "points/s",
+            "e2e": {"value": Np_total / (te / e2e_steps / 1e3), "unit": "points/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": te / e2e_steps},
             "gpu_launches": OUR_KERNELS_PER_STEP * args.steps,
@@ -286,6 +300,7 @@ def run_ours(args, cfg):
         }
     plan.close()
     if ws > 1:
+        comm.close()
         torch.distributed.destroy_process_group()
     return out
 
@@ -336,7 +351,7 @@ def run_reference(args, cfg):
     return {
         "impl": "reference", "metric": "NUFFT points/s (setpts + type-1 spread + type-2 interp per point)",
         "value": v, "unit": "points/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{cfg['name']}: {cfg['prec']} {N[0]}x{N[1]}x{N[2]} modes, "
                                f"{cfg['Np']} {cfg['kind']} points, eps={cfg['eps']:g}",
