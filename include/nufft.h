@@ -138,13 +138,35 @@ int nufft_get_info(nufft_handle h, nufft_info* info);
 /* Static string for a status code (host). */
 const char* nufft_strerror(int code);
 
-/* ---- multi-GPU bootstrap (one process per GPU; slab decomposition along z) ----
- * PyTorch only carries the 128-byte id through its process group. */
+/* ---- multi-GPU (one process per GPU; z-slab decomposition, §2.4) ----
+ * nufft_comm_unique_id: rank 0 makes the 128-byte NCCL id (host); PyTorch only carries
+ * it through its process group.  nufft_comm_init: collective over the nranks processes;
+ * *comm is passed as opts.comm to nufft_plan; the caller destroys it after its plans.
+ * A slab plan (opts.comm != NULL) needs nranks >= 2, 2 N3 and N2 divisible by nranks
+ * and 2 N3 / nranks >= ceil(w/2).  Rank r owns fine z-planes [r 2N3/P, (r+1) 2N3/P);
+ * nufft_setpts then moves every point to the rank owning its fine z-cell (unless
+ * opts.points_owned) and type 2 returns values to the caller's rank and order.
+ * Errors: NUFFT_ERR_NCCL for a failed NCCL call, NUFFT_ERR_UNSUPPORTED for a shape
+ * that cannot be slab-decomposed.  nufft_spread / nufft_interp are single-GPU only. */
 int nufft_comm_unique_id(char id[128]);                                    /* rank 0, host */
 int nufft_comm_init(const char id[128], int nranks, int rank, void** comm); /* collective   */
 int nufft_comm_destroy(void* comm);
-/* Distributed mode layout: this rank's [lo, hi) range of centered mode indices per axis. */
+/* This rank's [lo, hi) range of mode STORAGE indices per axis (x, y, z): the whole
+ * N1 N2 N3 block on one GPU; on a slab plan all of x and z and the y-slab
+ * [r N2/P, (r+1) N2/P).  fk arguments of a slab plan are that block, x fastest. */
 int nufft_local_modes(nufft_handle h, int64_t lo[3], int64_t hi[3]);
+
+/* ---- Particle-in-Fourier step helpers (§4) ----
+ * DEVICE pointers only; stream-ordered on the plan stream; precision of the plan. */
+/* Gauss's law in Fourier space on this rank's mode block (nufft_local_modes layout):
+ *   E_k = -i k rho_k / |k|^2, k = 2 pi n / L, E_0 = 0.  rho_k, ex_k, ey_k, ez_k: complex. */
+int nufft_pif_poisson(nufft_handle h, const void* rho_k, void* ex_k, void* ey_k, void* ez_k);
+/* Leapfrog kick of one velocity component: v[j] += scale * Re(e[j]), j < Np (e complex,
+ * e.g. a type-2 output; scale = (q/m) dt / L^3). */
+int nufft_pif_kick(nufft_handle h, int64_t Np, void* v, const void* e, double scale);
+/* Drift: x += v dt on each axis, folded onto [0, L). */
+int nufft_pif_drift(nufft_handle h, int64_t Np, void* x, void* y, void* z, const void* vx,
+                    const void* vy, const void* vz, double dt);
 
 #ifdef __cplusplus
 }

@@ -28,7 +28,7 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler",
           "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 CU_FLAGS = ARCH + COMMON + ["--expt-relaxed-constexpr", "-Xptxas", "-v"]
 
-SOURCES = ["sort.cu", "spread.cu", "spread_rows.cu", "interp.cu", "elementwise.cu",
+SOURCES = ["sort.cu", "spread.cu", "spread_rows.cu", "interp.cu", "elementwise.cu", "pif.cu",
            "dist_kernels.cu", "plan.cpp", "dist.cpp"]
 
 

@@ -622,4 +622,55 @@ int nufft_local_modes(nufft_handle p, int64_t lo[3], int64_t hi[3]) {
     return NUFFT_OK;
 }
 
+int nufft_pif_poisson(nufft_handle p, const void* rho_k, void* ex_k, void* ey_k, void* ez_k) {
+    cudaGetLastError();
+    if (!p || !rho_k || !ex_k || !ey_k || !ez_k) return NUFFT_ERR_ARG;
+    if (!is_device_ptr(rho_k) || !is_device_ptr(ex_k) || !is_device_ptr(ey_k) || !is_device_ptr(ez_k))
+        return NUFFT_ERR_ARG;
+    int64_t lo[3], hi[3];
+    nufft_local_modes(p, lo, hi);
+    if (p->prec == NUFFT_F64)
+        NUFFT_CK(launch_pif_poisson<double>(static_cast<const double2*>(rho_k), p->N, lo, hi,
+                                            p->geom.L, p->modeord, static_cast<double2*>(ex_k),
+                                            static_cast<double2*>(ey_k), static_cast<double2*>(ez_k),
+                                            p->stream));
+    else
+        NUFFT_CK(launch_pif_poisson<float>(static_cast<const float2*>(rho_k), p->N, lo, hi,
+                                           p->geom.L, p->modeord, static_cast<float2*>(ex_k),
+                                           static_cast<float2*>(ey_k), static_cast<float2*>(ez_k),
+                                           p->stream));
+    return NUFFT_OK;
+}
+
+int nufft_pif_kick(nufft_handle p, int64_t Np, void* v, const void* e, double scale) {
+    cudaGetLastError();
+    if (!p || Np < 0 || (Np > 0 && (!v || !e))) return NUFFT_ERR_ARG;
+    if (Np > 0 && (!is_device_ptr(v) || !is_device_ptr(e))) return NUFFT_ERR_ARG;
+    if (p->prec == NUFFT_F64)
+        NUFFT_CK(launch_pif_kick<double>(Np, static_cast<double*>(v), static_cast<const double2*>(e),
+                                         scale, p->stream));
+    else
+        NUFFT_CK(launch_pif_kick<float>(Np, static_cast<float*>(v), static_cast<const float2*>(e),
+                                        scale, p->stream));
+    return NUFFT_OK;
+}
+
+int nufft_pif_drift(nufft_handle p, int64_t Np, void* x, void* y, void* z, const void* vx,
+                    const void* vy, const void* vz, double dt) {
+    cudaGetLastError();
+    if (!p || Np < 0 || (Np > 0 && (!x || !y || !z || !vx || !vy || !vz))) return NUFFT_ERR_ARG;
+    if (Np > 0 && !is_device_ptr(x)) return NUFFT_ERR_ARG;
+    if (p->prec == NUFFT_F64)
+        NUFFT_CK(launch_pif_drift<double>(Np, static_cast<double*>(x), static_cast<double*>(y),
+                                          static_cast<double*>(z), static_cast<const double*>(vx),
+                                          static_cast<const double*>(vy),
+                                          static_cast<const double*>(vz), dt, p->geom.L, p->stream));
+    else
+        NUFFT_CK(launch_pif_drift<float>(Np, static_cast<float*>(x), static_cast<float*>(y),
+                                         static_cast<float*>(z), static_cast<const float*>(vx),
+                                         static_cast<const float*>(vy),
+                                         static_cast<const float*>(vz), dt, p->geom.L, p->stream));
+    return NUFFT_OK;
+}
+
 }  // extern "C"

@@ -122,6 +122,19 @@ void dist_destroy(nufft_plan_s* p);
 int dist_local_modes(nufft_plan_s* p, int64_t lo[3], int64_t hi[3]);
 int64_t dist_user_np(nufft_plan_s* p);  // points the caller passed (before redistribution)
 
+// pif.cu launchers
+template <typename T>
+cudaError_t launch_pif_poisson(const typename Cx<T>::type* rho, const int64_t N[3],
+                               const int64_t lo[3], const int64_t hi[3], double L, int modeord,
+                               typename Cx<T>::type* ex, typename Cx<T>::type* ey,
+                               typename Cx<T>::type* ez, cudaStream_t s);
+template <typename T>
+cudaError_t launch_pif_kick(int64_t Np, T* v, const typename Cx<T>::type* e, double s,
+                            cudaStream_t st);
+template <typename T>
+cudaError_t launch_pif_drift(int64_t Np, T* x, T* y, T* z, const T* vx, const T* vy, const T* vz,
+                             double dt, double L, cudaStream_t s);
+
 // dist_kernels.cu launchers
 template <typename T>
 cudaError_t launch_owner_count(int64_t Np, const T* z, double L, double scale, int64_t nf3,

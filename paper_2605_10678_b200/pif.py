@@ -1,0 +1,107 @@
+"""Particle-in-Fourier Landau damping on the NUFFT plan (§4).
+
+One step: (1) scatter the charges to Fourier space with a
+type-1 NUFFT, (2) solve Gauss's law E_k = -i k rho_k / |k|^2 (E_0 = 0),
+(3) gather each E component at the particles with a type-2 NUFFT, (4) leapfrog
+kick v += (q/m) dt Re E / L^3 and drift x += v dt (folded onto [0, L)).
+Plasma units, electrons q/m = -1, total charge Q_e = -L^3, L = 2 pi / k
+(SPEC.md:660-665 for the Poisson/push conventions).  Every
+arithmetic step runs in libnufft kernels (type 1/2, nufft_pif_poisson,
+nufft_pif_kick, nufft_pif_drift); this class holds buffers and calls them.
+
+With a Comm the plan is a z-slab plan: each rank samples ITS slab's share of
+the Landau distribution (z conditioned on the slab), points keep being owned by
+the rank that created them, and setpts moves only the ones that crossed a slab
+boundary to their current owner for the transforms (results come back).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+
+import torch
+
+from . import nufft as _n
+
+
+class LandauPIF:
+    def __init__(self, N, Np, eps=1e-4, dt=0.01, alpha=0.05, k=0.5, precision="f64",
+                 comm=None, device=None, seed=1, timing=False):
+        import synthetic
+        self.N = tuple(N)
+        self.k, self.alpha, self.dt = k, alpha, dt
+        self.L = 2 * math.pi / k
+        self.qm = -1.0
+        self.plan = _n.Plan(N, eps, precision=precision, L=self.L, comm=comm, device=device,
+                            timing=timing)
+        dev = self.plan.device
+        rdt, cdt = self.plan.real, self.plan.cplx
+        self.Np_total = int(Np)
+        if comm is None:
+            self.Np = int(Np)
+            pts = synthetic.landau_points(self.Np, alpha=alpha, k=k, seed=seed, device=dev, dtype=rdt)
+        else:
+            P, r = comm.size, comm.rank
+            nf3 = 2 * N[2]
+            z0, z1 = self.L * r / P, self.L * (r + 1) / P       # slab r of the fine grid
+            f0, f1 = synthetic.landau_cdf(z0, alpha, k), synthetic.landau_cdf(z1, alpha, k)
+            bounds = [round(Np * synthetic.landau_cdf(self.L * q / P, alpha, k) / self.L)
+                      for q in range(P + 1)]
+            self.Np = bounds[r + 1] - bounds[r]
+            assert nf3 % P == 0 and f1 > f0
+            pts = synthetic.landau_points(self.Np, alpha=alpha, k=k, seed=seed + 7919 * r,
+                                          device=dev, dtype=rdt, z_range=(z0, z1))
+        self.x, self.y, self.z = (p.contiguous() for p in pts)
+        vel = synthetic.maxwellian_velocities(self.Np, seed=seed + 4 + 104729 * (comm.rank if comm else 0),
+                                              device=dev, dtype=rdt)
+        self.vx, self.vy, self.vz = (v.contiguous() for v in vel)
+        self.q = -self.L ** 3 / self.Np_total              # Q_e = -L^3 shared equally
+        self.charge = torch.full((self.Np,), self.q, dtype=cdt, device=dev)
+        shape = self.plan.local_shape
+        self.rho_k = torch.empty(shape, dtype=cdt, device=dev)
+        self.e_k = [torch.empty(shape, dtype=cdt, device=dev) for _ in range(3)]
+        self.e_pts = torch.empty(self.Np, dtype=cdt, device=dev)
+        self.t = 0.0
+
+    def step(self):
+        p, L = self.plan, _n.lib()
+        with torch.cuda.device(p.device):
+            p.setpts(self.x, self.y, self.z)                                   # sort
+            p.type1(self.charge, out=self.rho_k)                               # (1) scatter
+            _n._check(L.nufft_pif_poisson(p._h, self.rho_k.data_ptr(), *(e.data_ptr() for e in self.e_k)),
+                      "nufft_pif_poisson")                                      # (2) field solve
+            s = self.qm * self.dt / self.L ** 3
+            for e_k, v in zip(self.e_k, (self.vx, self.vy, self.vz)):
+                p.type2(e_k, out=self.e_pts)                                    # (3) gather
+                _n._check(L.nufft_pif_kick(p._h, self.Np, ctypes.c_void_p(v.data_ptr()),
+                                           ctypes.c_void_p(self.e_pts.data_ptr()), ctypes.c_double(s)),
+                          "nufft_pif_kick")                                     # (4) push
+            _n._check(L.nufft_pif_drift(p._h, self.Np, *(ctypes.c_void_p(a.data_ptr()) for a in
+                                                         (self.x, self.y, self.z, self.vx, self.vy, self.vz)),
+                                        ctypes.c_double(self.dt)), "nufft_pif_drift")
+        self.t += self.dt
+
+    def field_energy(self) -> float:
+        """0.5 int |E|^2 dx = 0.5 L^-3 sum_k |E_k|^2 (this rank's modes; all-reduce for a slab plan)."""
+        w = sum(float((e.abs() ** 2).sum()) for e in self.e_k) * 0.5 / self.L ** 3
+        if self.plan.comm is not None:
+            import torch.distributed as dist
+            t = torch.tensor([w], dtype=torch.float64, device=self.plan.device)
+            dist.all_reduce(t)
+            w = float(t.item())
+        return w
+
+    def mode_amplitude(self, n=(1, 0, 0)) -> float:
+        """|E_x|-component amplitude of one mode n (centered storage), summed over ranks."""
+        lo, hi = self.plan.local_modes()
+        idx = [n[d] + self.N[d] // 2 for d in range(3)]
+        val = 0.0
+        if all(lo[d] <= idx[d] < hi[d] for d in range(3)):
+            e = self.e_k[0][idx[2] - lo[2], idx[1] - lo[1], idx[0] - lo[0]]
+            val = float(e.abs())
+        if self.plan.comm is not None:
+            import torch.distributed as dist
+            t = torch.tensor([val], dtype=torch.float64, device=self.plan.device)
+            dist.all_reduce(t)
+            val = float(t.item())
+        return val

@@ -84,18 +84,28 @@ def uniform_points(Np: int, L: float = 2 * math.pi, seed: int = 1, device="cpu",
     return tuple(pts)
 
 
+def landau_cdf(x: float, alpha: float = 0.05, k: float = 0.5) -> float:
+    """L * F(x) = x + (alpha/k) sin(k x): the unnormalised per-axis CDF."""
+    return x + (alpha / k) * math.sin(k * x)
+
+
 def landau_points(Np: int, alpha: float = 0.05, k: float = 0.5, seed: int = 1, device="cpu",
-                  dtype=torch.float64, newton_iters: int = 30):
+                  dtype=torch.float64, newton_iters: int = 30, z_range=None):
     """Per-axis inverse-CDF sampling of (1 + alpha cos(k x)) on [0, L), L = 2 pi / k.
 
     PAPER.md:502-508 (Landau damping initial distribution).  CDF:
     F(x) = (x + (alpha/k) sin(k x)) / L; solve F(x) = u by Newton from x0 = u L
     (F' >= (1 - alpha)/L > 0, so the iteration is monotone and converges).
+    z_range = (z0, z1) restricts z to that slab (conditional distribution), for
+    ranks that generate their own slab's particles.
     """
     L = 2 * math.pi / k
     pts = []
     for d in range(3):
         target = u01(seed, d, Np, device=device) * L
+        if d == 2 and z_range is not None:
+            f0, f1 = landau_cdf(z_range[0], alpha, k), landau_cdf(z_range[1], alpha, k)
+            target = f0 + target * ((f1 - f0) / L)
         x = target.clone()
         for _ in range(newton_iters):
             f = x + (alpha / k) * torch.sin(k * x) - target
