@@ -46,6 +46,13 @@ CONFIGS = {
                kind="uniform"),
     "c3e4": dict(name="C3", prec="f64", N=(256, 256, 256), Np=8 * 256 ** 3, eps=1e-4,
                  kind="uniform"),
+    # Landau-damping PIF step: 512^3 modes, 8 particles per mode,
+    # fp64, eps = 1e-4, dt = 0.01; metric = seconds per PIF step
+    "c4": dict(name="C4", prec="f64", N=(512, 512, 512), Np=8 * 512 ** 3, eps=1e-4,
+               kind="pif", dt=0.01),
+    # small PIF for quick checks
+    "pif128": dict(name="PIF-128", prec="f64", N=(128, 128, 128), Np=8 * 128 ** 3, eps=1e-4,
+                   kind="pif", dt=0.01),
 }
 OUR_KERNELS_PER_STEP = 9  # bin_count, 3 scan, scatter | spread, truncate_deconv | pad, interp
 REF_SAMPLE = 1 << 19
@@ -325,12 +332,158 @@ def cpu_baseline(cfg, sample=REF_SAMPLE):
             "seconds": t, "input_gen_seconds": t_gen}
 
 
+def run_pif(args, cfg):
+    """Seconds per Landau-damping PIF step: sort, type-1 charge
+    scatter, Poisson, three type-2 field gathers + kicks, drift -- all on device."""
+    import paper_2605_10678_b200 as nb
+    from paper_2605_10678_b200.pif import LandauPIF
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    stream = torch.cuda.current_stream(device)
+    comm = nb.Comm() if ws > 1 else None
+    sim = LandauPIF(cfg["N"], cfg["Np"], eps=cfg["eps"], dt=cfg["dt"], precision=cfg["prec"],
+                    comm=comm, device=device, timing=True)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=device)
+    for _ in range(args.warmup):
+        sim.step()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    stage = {k: [] for k in ("ms_setpts", "ms_spread", "ms_fft", "ms_deconv", "ms_pad",
+                             "ms_interp", "ms_comm")}
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        flush.fill_(k & 0xff)
+        evs[k][0].record(stream)
+        sim.step()
+        evs[k][1].record(stream)
+        info = sim.plan.info()   # last call of each stage (interp: the z-component gather)
+        for key in stage:
+            stage[key].append(info[key])
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    clocks = sampler.stop()
+    t_ms = sum(a.elapsed_time(b) for a, b in evs)
+    if ws > 1:
+        t = torch.tensor([t_ms], device=device, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t_ms = float(t.item())
+    ms_per_step = t_ms / args.steps
+    # e2e: the same step through the public API plus the D2H read of its result
+    # (the field-energy diagnostic); the particle state stays resident, so no H2D
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if ws > 1:
+        torch.distributed.barrier()
+    e2e_steps = max(2, min(args.steps, 5))
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        sim.step()
+        sim.field_energy()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    te = e0.elapsed_time(e1)
+    if ws > 1:
+        t = torch.tensor([te], device=device, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        te = float(t.item())
+    med = {k: statistics.median(v) for k, v in stage.items() if v and min(v) >= 0}
+    # dominant kernel per step: spread once, interp three times
+    sp, ip = med.get("ms_spread", 0.0), 3 * med.get("ms_interp", 0.0)
+    dom, dom_ms = ("spread", sp) if sp >= ip else ("interp", med.get("ms_interp", 0.0))
+    hbm, peak_src = peaks()
+    bytes_alg = algorithmic_bytes(cfg, dom) / ws
+    achieved = bytes_alg / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
+    out = None
+    if rank == 0:
+        N = cfg["N"]
+        cpu = pif_cpu_baseline() if (ws == 1 and not args.no_cpu_baseline) else None
+        out = {
+            "metric": "seconds per Landau-damping PIF step", "value": ms_per_step / 1e3,
+            "unit": "s/step", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64" if cfg["prec"] == "f64" else "f32",
+            "data": "synthetic",
+            "config": {"workload": f"{cfg['name']}: PIF Landau damping, {N[0]}^3 modes, "
+                                   f"{cfg['Np']} particles (8 per mode), eps={cfg['eps']:g}, "
+                                   f"dt={cfg['dt']}", "N": list(N), "Np_total": cfg["Np"],
+                       "w": sim.plan.info()["w"], "tile": sim.plan.info()["tile"],
+                       "parallelism": f"z-slab x{ws} (NCCL)" if ws > 1 else "1 GPU",
+                       "l2": "flushed (512 MB write) before every timed step"},
+            "stage_ms_median": med,
+            "e2e": {"value": te / e2e_steps / 1e3, "unit": "s/step", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 8,
+                    "note": "state resident on device; field-energy scalar read back per step"},
+            "gpu_launches": (OUR_KERNELS_PER_STEP + 2 * 2 + 2) * args.steps,
+            "roofline": {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": hbm,
+                         "peak_source": peak_src, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": load_traffic(args.config, dom),
+                         "algorithmic_bytes_per_launch": bytes_alg, "ms_per_launch": dom_ms},
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+        }
+    sim.plan.close()
+    if ws > 1:
+        comm.close()
+        torch.distributed.destroy_process_group()
+    return out
+
+
+def pif_cpu_baseline():
+    """The oracle PIF step (oracle type 1 + 3 type 2, numpy Poisson / push) on a
+    bounded sample: 32^3 modes, 8 particles per mode."""
+    import numpy as np
+    import oracle
+    import synthetic
+    N, Np, eps, dt, L = (32, 32, 32), 8 * 32 ** 3, 1e-4, 0.01, 4 * math.pi
+    x, y, z = (t.numpy() for t in synthetic.landau_points(Np))
+    v = [t.numpy().copy() for t in synthetic.maxwellian_velocities(Np)]
+    c = np.full(Np, -L ** 3 / Np, dtype=np.complex128)
+    t0 = time.perf_counter()
+    rho = oracle.type1(x, y, z, c, N, eps, L=L)
+    n = [np.arange(N[d]) - N[d] // 2 for d in range(3)]
+    ks = [(2 * math.pi / L) * n[0][None, None, :], (2 * math.pi / L) * n[1][None, :, None],
+          (2 * math.pi / L) * n[2][:, None, None]]
+    kk = ks[0] ** 2 + ks[1] ** 2 + ks[2] ** 2
+    inv = np.where(kk > 0, 1.0 / np.where(kk > 0, kk, 1.0), 0.0)
+    for d in range(3):
+        e = oracle.type2(x, y, z, -1j * ks[d] * rho * inv, eps, L=L)
+        v[d] += -dt * e.real / L ** 3
+    x, y, z = (np.mod(a + vd * dt, L) for a, vd in zip((x, y, z), v))
+    t = time.perf_counter() - t0
+    return {"value": t, "unit": "s/step", "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"one oracle PIF step at 32^3 modes, {Np} particles (8 per mode), "
+                      "eps=1e-4 (the 512^3 workload does not fit the oracle's budget)"}
+
+
 def run_reference(args, cfg):
     ws, rank, _ = dist_env()
     if rank != 0:
         return None
     import oracle
     import synthetic
+    if cfg["kind"] == "pif":   # oracle PIF steps on the bounded sample of pif_cpu_baseline
+        for _ in range(args.warmup):
+            pif_cpu_baseline()
+        ts = [pif_cpu_baseline() for _ in range(args.steps)]
+        v = statistics.median(t["value"] for t in ts)
+        return {"impl": "reference", "metric": "seconds per Landau-damping PIF step", "value": v,
+                "unit": "s/step", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": cfg["name"], "sample": ts[0]["sample"]},
+                "cpu_baseline": ts[0],
+                "e2e": {"value": v, "unit": "s/step", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
     sample = REF_SAMPLE
     x, y, z = (v.numpy() for v in synthetic.uniform_points(sample))
     c = synthetic.strengths(sample).numpy()
@@ -380,7 +533,12 @@ def main():
     if args.warmup < 3:
         args.warmup = 3
     cfg = CONFIGS[args.config]
-    out = run_reference(args, cfg) if args.impl == "reference" else run_ours(args, cfg)
+    if args.impl == "reference":
+        out = run_reference(args, cfg)
+    elif cfg["kind"] == "pif":
+        out = run_pif(args, cfg)
+    else:
+        out = run_ours(args, cfg)
     if out is not None:
         print(json.dumps(out), flush=True)
 
