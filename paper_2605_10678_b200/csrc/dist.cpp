@@ -83,10 +83,13 @@ int nccl_status(ncclResult_t r) { return r == ncclSuccess ? NUFFT_OK : NUFFT_ERR
         if (r__ != ncclSuccess) return NUFFT_ERR_NCCL;         \
     } while (0)
 
+// grow-only staging buffers with 12.5 % slack: per-step particle migration changes
+// the counts slightly, and a cudaFree/cudaMalloc of GBs every step would dominate
 int ensure(nufft_plan_s* p, void** buf, size_t* have, size_t need) {
     if (*have >= need && *buf) return NUFFT_OK;
     dev_free(p, buf, *have);
     *have = 0;
+    need += need / 8;
     int st = dev_alloc(p, buf, need);
     if (!st) *have = need;
     return st;
@@ -325,9 +328,10 @@ int dist_setpts(nufft_plan_s* p, int64_t Np, const void* x, const void* y, const
         dev_free(p, (void**)&d->owner, 4 * d->cap_user);
         dev_free(p, (void**)&d->rank_in, 4 * d->cap_user);
         d->cap_user = 0;
-        if ((st = dev_alloc(p, (void**)&d->owner, 4 * (size_t)Np))) return st;
-        if ((st = dev_alloc(p, (void**)&d->rank_in, 4 * (size_t)Np))) return st;
-        d->cap_user = Np;
+        const int64_t cap = Np + Np / 8;
+        if ((st = dev_alloc(p, (void**)&d->owner, 4 * (size_t)cap))) return st;
+        if ((st = dev_alloc(p, (void**)&d->rank_in, 4 * (size_t)cap))) return st;
+        d->cap_user = cap;
     }
     NUFFT_CK(cudaMemsetAsync(d->d_counts, 0, sizeof(unsigned long long) * P, p->stream));
     const Geom& g = p->geom;

@@ -169,7 +169,8 @@ int local_sort(nufft_plan_s* p, int64_t Np, const void* xd, const void* yd, cons
         dev_free(p, (void**)&p->rank_of, 4 * p->cap);
         dev_free(p, &p->rec, 32 * p->cap);
         p->cap = 0;
-        const size_t n = (size_t)Np;
+        // a slab plan's local count drifts step to step (migration): 6 % slack there
+        const size_t n = (size_t)(p->dist ? Np + Np / 16 : Np);
         st = dev_alloc(p, (void**)&p->bin_of, 4 * n);
         if (!st) st = dev_alloc(p, (void**)&p->rank_of, 4 * n);
         if (!st) st = dev_alloc(p, &p->rec, 32 * n);
@@ -177,7 +178,7 @@ int local_sort(nufft_plan_s* p, int64_t Np, const void* xd, const void* yd, cons
             p->Np = -1;
             return st;
         }
-        p->cap = Np;
+        p->cap = (int64_t)n;
     }
     if (p->prec == NUFFT_F64)
         NUFFT_CK(launch_bin_sort<double>(p->geom, Np, static_cast<const double*>(xd),
