@@ -28,8 +28,8 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler",
           "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 CU_FLAGS = ARCH + COMMON + ["--expt-relaxed-constexpr", "-Xptxas", "-v"]
 
-SOURCES = ["sort.cu", "spread.cu", "spread_rows.cu", "interp.cu", "elementwise.cu", "pif.cu",
-           "dist_kernels.cu", "plan.cpp", "dist.cpp"]
+SOURCES = ["sort.cu", "spread.cu", "spread_rows.cu", "spread_outer.cu", "interp.cu",
+           "elementwise.cu", "pif.cu", "dist_kernels.cu", "plan.cpp", "dist.cpp"]
 
 
 def _nccl_dirs():

@@ -29,7 +29,8 @@ struct Geom {
     double L;           // period
     double scale[3];    // nf / L
     int w;              // kernel width
-    int spread_warps;   // spread kernel: 1 = register rows, 4 / 8 = smem z-plane owners
+    int spread_warps;   // spread kernel: 1 = register rows, 2 = plane outer products,
+                        // 4 / 8 = smem z-plane owners
     // z boundary: 1 = periodic over nz_loc (one GPU); 0 = z-slab of a distributed
     // plan, the grid pointer addresses local plane 0 and planes [-hz_lo, nz_loc + hz_hi)
     // exist (ghost halos accumulated / filled over NCCL)
@@ -93,6 +94,13 @@ cudaError_t launch_spread_rows(const Geom& g, const PtsView<T>& p, int64_t nbins
                                const typename Cx<T>::type* c, typename Cx<T>::type* grid,
                                double beta, cudaStream_t s);
 template <typename T> size_t spread_rows_smem_bytes(const Geom& g);
+// spread_outer.cu: per-plane outer-product spread (w <= 12 and T = 16 - w on every axis)
+bool spread_outer_applies(const Geom& g);
+template <typename T>
+cudaError_t launch_spread_outer(const Geom& g, const PtsView<T>& p, int64_t nbins,
+                                const typename Cx<T>::type* c, typename Cx<T>::type* grid,
+                                double beta, cudaStream_t s);
+template <typename T> size_t spread_outer_smem_bytes(const Geom& g);
 template <typename T> size_t interp_smem_bytes(const Geom& g);
 // elementwise.cu
 template <typename T>

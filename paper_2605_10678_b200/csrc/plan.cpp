@@ -199,7 +199,16 @@ int local_sort(nufft_plan_s* p, int64_t Np, const void* xd, const void* yd, cons
 int do_spread(nufft_plan_s* p, const void* c_dev, void* grid0) {
     StageTimer tm(p, EV_SPREAD);
     const bool rows = p->geom.spread_warps == 1;  // register-row kernel (plan checked it applies)
-    if (rows && p->prec == NUFFT_F64)
+    const bool outer = p->geom.spread_warps == 2;  // plane outer-product kernel (ditto)
+    if (outer && p->prec == NUFFT_F64)
+        NUFFT_CK(launch_spread_outer<double>(p->geom, pts_view<double>(p), p->nbins,
+                                             static_cast<const double2*>(c_dev),
+                                             static_cast<double2*>(grid0), p->beta, p->stream));
+    else if (outer)
+        NUFFT_CK(launch_spread_outer<float>(p->geom, pts_view<float>(p), p->nbins,
+                                            static_cast<const float2*>(c_dev),
+                                            static_cast<float2*>(grid0), p->beta, p->stream));
+    else if (rows && p->prec == NUFFT_F64)
         NUFFT_CK(launch_spread_rows<double>(p->geom, pts_view<double>(p), p->nbins,
                                             static_cast<const double2*>(c_dev),
                                             static_cast<double2*>(grid0), p->beta, p->stream));
@@ -299,7 +308,8 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
     if (opts) o = *opts;
     else nufft_default_opts(&o);
     if (!(o.L > 0) || (o.modeord != 0 && o.modeord != 1)) return NUFFT_ERR_ARG;
-    if (o.spread_warps != 0 && o.spread_warps != 1 && o.spread_warps != 4 && o.spread_warps != 8)
+    if (o.spread_warps != 0 && o.spread_warps != 1 && o.spread_warps != 2 &&
+        o.spread_warps != 4 && o.spread_warps != 8)
         return NUFFT_ERR_ARG;
 
     nufft_plan_s* p = new (std::nothrow) nufft_plan_s();
@@ -349,7 +359,8 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
     g.spread_warps = o.spread_warps;
     if (g.spread_warps == 0)
         g.spread_warps = (precision == NUFFT_F32 && spread_rows_applies(g)) ? 1 : 8;
-    if (g.spread_warps == 1 && !spread_rows_applies(g)) {
+    if ((g.spread_warps == 1 && !spread_rows_applies(g)) ||
+        (g.spread_warps == 2 && !spread_outer_applies(g))) {
         delete p;
         return NUFFT_ERR_UNSUPPORTED;
     }
@@ -365,10 +376,15 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
             delete p;
             return NUFFT_ERR_CUDA;
         }
-        const bool rows = g.spread_warps == 1;
-        const size_t sp = precision == NUFFT_F64
-                              ? (rows ? spread_rows_smem_bytes<double>(g) : spread_smem_bytes<double>(g))
-                              : (rows ? spread_rows_smem_bytes<float>(g) : spread_smem_bytes<float>(g));
+        const bool rows = g.spread_warps == 1, outer = g.spread_warps == 2;
+        const size_t sp =
+            precision == NUFFT_F64
+                ? (outer  ? spread_outer_smem_bytes<double>(g)
+                   : rows ? spread_rows_smem_bytes<double>(g)
+                          : spread_smem_bytes<double>(g))
+                : (outer  ? spread_outer_smem_bytes<float>(g)
+                   : rows ? spread_rows_smem_bytes<float>(g)
+                          : spread_smem_bytes<float>(g));
         const size_t need = std::max(sp, precision == NUFFT_F64 ? interp_smem_bytes<double>(g)
                                                                 : interp_smem_bytes<float>(g));
         if (need > (size_t)smem_max) {

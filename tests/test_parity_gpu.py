@@ -142,14 +142,15 @@ def test_nonuniform_shape_signs_modeord_landau(nb):
 
 
 @pytest.mark.parametrize("prec", ["f64", "f32"])
-@pytest.mark.parametrize("kernel", [1, 4, 8])
+@pytest.mark.parametrize("kernel", [1, 2, 4, 8])
 @pytest.mark.parametrize("eps", [1e-3, 1e-6, 1e-9])
 def test_every_spread_kernel(nb, prec, kernel, eps):
-    # 1 = register-row spread (T = 16 - w), 4 / 8 = shared-memory z-plane owners
+    # 1 = register-row spread, 2 = plane outer products (both T = 16 - w),
+    # 4 / 8 = shared-memory z-plane owners
     if prec == "f32" and eps < 1e-7:
         eps = 1e-7
     w = nb.Plan((8, 8, 8), eps, precision=prec).info()["w"]
-    tile = 16 - w if kernel == 1 else 8
+    tile = 16 - w if kernel in (1, 2) else 8
     N, Np = (24, 24, 24), 20000
     pts, c = host_inputs(Np, prec, seed=11)
     fk = synthetic.modes(*N).to(c.dtype)
@@ -206,18 +207,21 @@ def test_edge_cases(nb):
         assert oracle.rel_l2(g2, oracle.type2(*pts, np64(fk), w_eps, L=L)) <= 1e-10
 
 
-def test_clustered_points_one_hot_bin(nb):
-    # all points in a few tiles (load imbalance) and all in ONE cell
+@pytest.mark.parametrize("kernel", [0, 1, 2, 8])
+def test_clustered_points_one_hot_bin(nb, kernel):
+    # all points in a few tiles (load imbalance, many batches per bin) and all in
+    # ONE cell; every spread kernel (w = 7: the register kernels take T = 9)
     N, Np, eps = (32, 32, 32), 50000, 1e-6
+    tile = 9 if kernel in (1, 2) else None
     pts, c = host_inputs(Np, "f64", kind="clustered")
     fk = synthetic.modes(*N)
     x, y, z = (np64(p) for p in pts)
-    _, g1, g2 = run_pair(nb, N, eps, "f64", pts, c, fk)
+    _, g1, g2 = run_pair(nb, N, eps, "f64", pts, c, fk, tile=tile, spread_warps=kernel)
     assert oracle.rel_l2(g1, oracle.type1(x, y, z, np64(c), N, eps)) <= 1e-10
     assert oracle.rel_l2(g2, oracle.type2(x, y, z, np64(fk), eps)) <= 1e-10
     one = tuple(torch.full((5000,), 1.2345, dtype=torch.float64) for _ in range(3))
     c1 = synthetic.strengths(5000)
-    _, g1, g2 = run_pair(nb, N, eps, "f64", one, c1, fk)
+    _, g1, g2 = run_pair(nb, N, eps, "f64", one, c1, fk, tile=tile, spread_warps=kernel)
     o = [np64(p) for p in one]
     assert oracle.rel_l2(g1, oracle.type1(*o, np64(c1), N, eps)) <= 1e-10
     assert oracle.rel_l2(g2, oracle.type2(*o, np64(fk), eps)) <= 1e-10
