@@ -244,12 +244,12 @@ int do_interp(nufft_plan_s* p, const void* grid0, void* c_dev) {
 
 namespace {
 
-// Default bin edge by width (measured on B200, profiles/README.md): fp32 uses the
-// register-row spread, whose subgrid is 16 x 16 x 16 cells (T = 16 - w); fp64 uses
-// the shared-memory z-plane spread with T = 8 up to w = 8 (subgrid <= 16^3 x 16 B
-// = 64 KB), T = 16 - w (>= 4) beyond; never larger than the grid allows.
+// Default bin edge by width (measured on B200, profiles/README.md): the register
+// outer-product spread takes a 16 x 16 x 16 subgrid (T = 16 - w) -- the default
+// for fp32 and for fp64 with w >= 6; fp64 with w <= 5 uses the shared-memory
+// z-plane spread with T = 8; never larger than the grid allows.
 int default_tile(int w, int prec, int64_t nf) {
-    int t = (prec == NUFFT_F64 && w <= 8) ? 8 : 16 - w;
+    int t = (prec == NUFFT_F64 && w <= 5) ? 8 : 16 - w;
     if (t < 4) t = 4;
     if (t > 64) t = 64;
     if (t > nf - w - 2) t = (int)(nf - w - 2);  // T + w + 2 <= nf: one-step periodic wraps, <= 2 row segments
@@ -353,12 +353,12 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
     g.zper = 1;
     g.hz_lo = 0;
     g.hz_hi = 0;
-    // spread kernel: 1 = register rows (needs w <= 12 and T = 16 - w), 4 / 8 = shared-
-    // memory z-plane owners with that many warps; 0 = rows for fp32 when they apply,
-    // else 8 z-plane owners (the faster pair on B200 per precision, profiles/README.md)
+    // spread kernel: 1 = register rows, 2 = register outer products (both need
+    // w <= 12 and T = 16 - w), 4 / 8 = shared-memory z-plane owners with that many
+    // warps; 0 = outer products when they apply, else 8 z-plane owners (the
+    // fastest on B200 per precision and width, profiles/README.md)
     g.spread_warps = o.spread_warps;
-    if (g.spread_warps == 0)
-        g.spread_warps = (precision == NUFFT_F32 && spread_rows_applies(g)) ? 1 : 8;
+    if (g.spread_warps == 0) g.spread_warps = spread_outer_applies(g) ? 2 : 8;
     if ((g.spread_warps == 1 && !spread_rows_applies(g)) ||
         (g.spread_warps == 2 && !spread_outer_applies(g))) {
         delete p;
