@@ -103,17 +103,26 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 }
 
 // Tile x-geometry shared by spread and interp.  Bulk copies need 16-byte
-// aligned rows: fp64 complex cells are 16 bytes, so any origin works (pitch =
-// T + w); fp32 complex cells are 8 bytes, so the subgrid row starts at an EVEN
-// global x and has an even pitch, round_up_even(T + w + 1).
+// aligned rows: fp64 complex cells are 16 bytes, so any origin works (row
+// length = pitch = T + w); fp32 complex cells are 8 bytes, so the subgrid row
+// starts at an EVEN global x and has an even length round_up_even(T + w + 1),
+// and the smem pitch is = 8 (mod 16) cells: two consecutive rows of 8 cells then
+// fill one 128-byte wavefront of 64-bit loads without bank conflicts.
 struct TileX {
     int gx0;    // global x of smem column 0 (may be negative: periodic)
     int shift;  // smem column of the nominal tile origin bx*T - w/2 (0 or 1)
-    int pitch;  // smem row length in cells
+    int len;    // cells per row copied to / from the grid
+    int pitch;  // smem row stride in cells (>= len)
 };
 template <int CELL_BYTES>
-__host__ __device__ __forceinline__ int tile_pitch(int T, int W) {
+__host__ __device__ __forceinline__ int tile_len(int T, int W) {
     return CELL_BYTES >= 16 ? T + W : ((T + W + 2) & ~1);
+}
+template <int CELL_BYTES>
+__host__ __device__ __forceinline__ int tile_pitch(int T, int W) {
+    const int len = tile_len<CELL_BYTES>(T, W);
+    if (CELL_BYTES >= 16) return len;
+    return len <= 8 ? 8 : 16 * ((len - 8 + 15) / 16) + 8;
 }
 template <int CELL_BYTES>
 __device__ __forceinline__ TileX tile_x(int bx, int T, int W) {
@@ -121,6 +130,7 @@ __device__ __forceinline__ TileX tile_x(int bx, int T, int W) {
     TileX t;
     t.shift = CELL_BYTES >= 16 ? 0 : (ox & 1);
     t.gx0 = ox - t.shift;
+    t.len = tile_len<CELL_BYTES>(T, W);
     t.pitch = tile_pitch<CELL_BYTES>(T, W);
     return t;
 }

@@ -16,7 +16,12 @@
 // PAPER.md:176), parking them in a per-warp shared buffer.  The warp then
 // walks the 32 points: lane slots cover the w x w (x, y) columns of the
 // stencil, each sums its w z-cells against wz, scales by wx*wy, and a shuffle
-// reduction yields c_j, written in the caller's order (c[perm[slot]]).
+// reduction yields c_j, written in the caller's order (c[perm[slot]]).  The
+// kernel is bound by shared-memory wavefronts (one 8- or 16-byte cell load per
+// stencil cell), so the slot map is chosen for them: for w >= 6 a quarter-warp
+// reads 8 consecutive cells of ONE row (x = lane % 8, y = lane / 8 + 4 pass),
+// conflict-free for any row pitch; for w <= 5 the flat map over the w^2 columns
+// wastes fewer lanes.
 #include "device_util.cuh"
 #include "internal.cuh"
 
@@ -43,7 +48,9 @@ __global__ void __launch_bounds__(kInterpThreads, 2)
     interp_tile_kernel(Geom g, PtsView<T> p, const typename Cx<T>::type* __restrict__ grid,
                        typename Cx<T>::type* __restrict__ out, T beta) {
     using C = typename Cx<T>::type;
-    constexpr int NQ = (W * W + 31) / 32;
+    constexpr bool kFlat = W <= 5;
+    constexpr int NQ = kFlat ? (W * W + 31) / 32 : 1;
+    constexpr int XS = W <= 8 ? 8 : 16, YS = 32 / XS, NPASS = (W + YS - 1) / YS;
     constexpr int WS = InterpSmem<T, W>::WS;
     constexpr int NW = kInterpWarps;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -66,14 +73,14 @@ __global__ void __launch_bounds__(kInterpThreads, 2)
     // ---- stage the subgrid with bulk copies (one mbarrier transaction)
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
-        mbar_arrive_expect_tx(bar, (unsigned)(ncell * sizeof(C)));
+        mbar_arrive_expect_tx(bar, (unsigned)(Ey * Ez * tx.len * sizeof(C)));
     }
     __syncthreads();
     {
         const int oy = by * g.T[1] - W / 2, oz = bz * g.T[2] - W / 2;
         const int nfx = (int)g.nf[0], nfy = (int)g.nf[1];
         int sg[2], ss[2], sn[2];
-        const int nseg = row_segments(tx.gx0, pitch, nfx, sg, ss, sn);
+        const int nseg = row_segments(tx.gx0, tx.len, nfx, sg, ss, sn);
         for (int r = threadIdx.x; r < Ey * Ez; r += kInterpThreads) {
             const int cz = r / Ey, cy = r - cz * Ey;
             int gz = z_row(oz + cz, g);
@@ -88,6 +95,10 @@ __global__ void __launch_bounds__(kInterpThreads, 2)
         }
     }
 
+    // lane slots.  w <= 5: flat slots s = lane + 32 q over the w x w columns
+    // (x = s % w, y = s / w); w >= 6: x = lane % XS, y = lane / XS + YS * pass
+    // (one 8-cell row per 128-bit quarter-warp phase: no bank conflicts)
+    const int sx = lane % XS, sy0 = lane / XS;
     int qoff[NQ], qx[NQ], qy[NQ];
     bool qok[NQ];
 #pragma unroll
@@ -141,22 +152,48 @@ __global__ void __launch_bounds__(kInterpThreads, 2)
                 if (j < np) {
                     const int base = __shfl_sync(0xffffffffu, my_base, j);
                     const T* wj = wb + j * WS;
+                    T wz[W];
 #pragma unroll
-                    for (int q = 0; q < NQ; ++q) {
-                        if (qok[q]) {
-                            const C* col = tile + base + qoff[q];
-                            T sr = 0, si = 0;
+                    for (int k = 0; k < W; ++k) wz[k] = wj[2 * W + k];
+                    if constexpr (kFlat) {
 #pragma unroll
-                            for (int k = 0; k < W; ++k) {
-                                const C v = col[k * plane];
-                                const T wz = wj[2 * W + k];
-                                sr += v.x * wz;
-                                si += v.y * wz;
+                        for (int q = 0; q < NQ; ++q) {
+                            if (qok[q]) {
+                                const C* col = tile + base + qoff[q];
+                                T sr = 0, si = 0;
+#pragma unroll
+                                for (int k = 0; k < W; ++k) {
+                                    const C v = col[k * plane];
+                                    sr += v.x * wz[k];
+                                    si += v.y * wz[k];
+                                }
+                                const T wxy = wj[qx[q]] * wj[W + qy[q]];
+                                vr[g4] += sr * wxy;
+                                vi[g4] += si * wxy;
                             }
-                            const T wxy = wj[qx[q]] * wj[W + qy[q]];
-                            vr[g4] += sr * wxy;
-                            vi[g4] += si * wxy;
                         }
+                    } else {
+                        const C* col0 = tile + base + sx;
+#pragma unroll
+                        for (int ps = 0; ps < NPASS; ++ps) {
+                            const int y = sy0 + YS * ps;
+                            if (sx < W && y < W) {
+                                const C* col = col0 + y * pitch;
+                                T sr = 0, si = 0;
+#pragma unroll
+                                for (int k = 0; k < W; ++k) {
+                                    const C v = col[k * plane];
+                                    sr += v.x * wz[k];
+                                    si += v.y * wz[k];
+                                }
+                                const T wy = wj[W + y];
+                                vr[g4] += sr * wy;
+                                vi[g4] += si * wy;
+                            }
+                        }
+                        const T wx = sx < W ? wj[sx] : (T)0;
+                        vr[g4] *= wx;
+                        vi[g4] *= wx;
                     }
                 }
             }

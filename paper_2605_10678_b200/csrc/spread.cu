@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(32 * NW)
     const int oy = by * g.T[1] - W / 2, oz = bz * g.T[2] - W / 2;
     const int nfx = (int)g.nf[0], nfy = (int)g.nf[1];
     int sg[2], ss[2], sn[2];
-    const int nseg = row_segments(tx.gx0, pitch, nfx, sg, ss, sn);
+    const int nseg = row_segments(tx.gx0, tx.len, nfx, sg, ss, sn);
     for (int r = threadIdx.x; r < Ey * Ez; r += kSpreadThreads) {
         const int cz = r / Ey, cy = r - cz * Ey;
         const int gy = wrap1(oy + cy, nfy), gz = z_row(oz + cz, g);
