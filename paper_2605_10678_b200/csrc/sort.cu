@@ -26,9 +26,13 @@ constexpr int kScanThreads = 1024;
 constexpr int kScanItems = 4;                        // per thread
 constexpr int kScanTile = kScanThreads * kScanItems;  // counts per scan tile
 
-// Fold onto [0, L) and rescale to fine-grid units (reading R10), fp64.
+constexpr int kScatterILP = 4;  // points per thread per scatter round
+
+// Fold onto [0, L) and rescale to fine-grid units (reading R10), fp64.  For x in
+// [0, L) the quotient x / L rounds to at most 1 - 2^-53, so floor(x / L) = 0 and
+// the fold is the identity: the fp64 division runs only for x outside [0, L).
 __device__ __forceinline__ double fold_rescale(double x, double L, double scale, int64_t nf) {
-    double xf = x - L * floor(x / L);
+    double xf = (x >= 0.0 && x < L) ? x : x - L * floor(x / L);
     double s = xf * scale;
     if (s >= (double)nf) s -= (double)nf;
     if (s < 0.0) s += (double)nf;
@@ -174,6 +178,16 @@ __device__ __forceinline__ void local_stencil(double s, int c, int T, int w, int
     *d = ls - a;
 }
 
+// one sorted record: two 16-byte streaming stores (.cs: written once, read by
+// the next kernel from HBM; do not keep it in L1)
+template <typename T>
+__device__ __forceinline__ void store_rec_stream(PtRec<T>* dst, const PtRec<T>& r) {
+    const int4* s = reinterpret_cast<const int4*>(&r);
+    int4* d = reinterpret_cast<int4*>(dst);
+    __stcs(d, s[0]);
+    __stcs(d + 1, s[1]);
+}
+
 // slot = offset[bin] + rank; the whole 32-byte record (one full DRAM sector,
 // two 16-byte stores) goes to the slot: the only random access of setpts.
 template <typename T>
@@ -182,27 +196,50 @@ __global__ void __launch_bounds__(kSortThreads) scatter_kernel(
     const T* __restrict__ z, const uint32_t* __restrict__ bin_of,
     const uint32_t* __restrict__ rank_of, const uint32_t* __restrict__ offset,
     PtRec<T>* __restrict__ rec) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < Np;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t slot = offset[bin_of[i]] + rank_of[i];
-        const double sx = fold_rescale((double)x[i], g.L, g.scale[0], g.nf[0]);
-        const double sy = fold_rescale((double)y[i], g.L, g.scale[1], g.nf[1]);
-        double sz = fold_rescale((double)z[i], g.L, g.scale[2], g.nf[2]) - (double)g.z_lo;
-        if (!(sz >= 0.0)) sz = 0.0;  // outside the slab: clamp (see bin_count_kernel)
-        if (sz >= (double)g.nz_loc) sz = (double)g.nz_loc - 0.5;
-        int lax, lay, laz;
-        double ddx, ddy, ddz;
-        local_stencil(sx, cell_of(sx, g.nf[0]), g.T[0], g.w, &lax, &ddx);
-        local_stencil(sy, cell_of(sy, g.nf[1]), g.T[1], g.w, &lay, &ddy);
-        local_stencil(sz, cell_of(sz + (double)g.z_lo, g.nf[2]) - (int)g.z_lo, g.T[2], g.w, &laz,
-                      &ddz);
-        PtRec<T> r;
-        r.d[0] = (T)ddx;
-        r.d[1] = (T)ddy;
-        r.d[2] = (T)ddz;
-        r.la = (uint32_t)lax | ((uint32_t)lay << 8) | ((uint32_t)laz << 16);
-        r.perm = (uint32_t)i;
-        rec[slot] = r;
+    // kScatterILP points per thread per round, every load issued before any use:
+    // the dependent offset[bin] lookups and the random stores overlap across points
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < Np;
+         i0 += kScatterILP * stride) {
+        uint32_t slot[kScatterILP];
+        T xv[kScatterILP], yv[kScatterILP], zv[kScatterILP];
+#pragma unroll
+        for (int u = 0; u < kScatterILP; ++u) {
+            const int64_t i = i0 + u * stride;
+            const bool ok = i < Np;
+            slot[u] = ok ? bin_of[i] : 0u;
+            xv[u] = ok ? x[i] : (T)0;
+            yv[u] = ok ? y[i] : (T)0;
+            zv[u] = ok ? z[i] : (T)0;
+        }
+#pragma unroll
+        for (int u = 0; u < kScatterILP; ++u) {
+            const int64_t i = i0 + u * stride;
+            if (i < Np) slot[u] = offset[slot[u]] + rank_of[i];
+        }
+#pragma unroll
+        for (int u = 0; u < kScatterILP; ++u) {
+            const int64_t i = i0 + u * stride;
+            if (i >= Np) break;
+            const double sx = fold_rescale((double)xv[u], g.L, g.scale[0], g.nf[0]);
+            const double sy = fold_rescale((double)yv[u], g.L, g.scale[1], g.nf[1]);
+            double sz = fold_rescale((double)zv[u], g.L, g.scale[2], g.nf[2]) - (double)g.z_lo;
+            if (!(sz >= 0.0)) sz = 0.0;  // outside the slab: clamp (see bin_count_kernel)
+            if (sz >= (double)g.nz_loc) sz = (double)g.nz_loc - 0.5;
+            int lax, lay, laz;
+            double ddx, ddy, ddz;
+            local_stencil(sx, cell_of(sx, g.nf[0]), g.T[0], g.w, &lax, &ddx);
+            local_stencil(sy, cell_of(sy, g.nf[1]), g.T[1], g.w, &lay, &ddy);
+            local_stencil(sz, cell_of(sz + (double)g.z_lo, g.nf[2]) - (int)g.z_lo, g.T[2], g.w,
+                          &laz, &ddz);
+            PtRec<T> r;
+            r.d[0] = (T)ddx;
+            r.d[1] = (T)ddy;
+            r.d[2] = (T)ddz;
+            r.la = (uint32_t)lax | ((uint32_t)lay << 8) | ((uint32_t)laz << 16);
+            r.perm = (uint32_t)i;
+            store_rec_stream(&rec[slot[u]], r);
+        }
     }
 }
 
