@@ -37,7 +37,10 @@ constexpr int kInterpWarps = kInterpThreads / 32;
 template <typename T, int W>
 struct InterpSmem {
     using C = typename Cx<T>::type;
-    static constexpr int WS = 3 * W + 1;  // per-point weight stride (odd: fewer bank conflicts)
+    // per-point weight stride in elements, ODD: lane l stores its point's weights
+    // at l * WS, so the 32 (fp32) / 16 (fp64 half-warp) lanes of a store hit
+    // distinct banks (an even stride such as 16 at w = 5 serialises them 16-32 way)
+    static constexpr int WS = (3 * W + 1) | 1;
     static size_t bytes(int ncell) {
         return (size_t)ncell * sizeof(C) + (size_t)kInterpWarps * 32 * WS * sizeof(T) + 16;
     }
