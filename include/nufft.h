@@ -73,7 +73,8 @@ typedef struct {
     int points_owned;  /* distributed: 1 = caller guarantees each point lies in this rank's z-slab   */
     int tile[3];       /* bin edge T_d (fine cells); 0 = built-in table by w; T_d + w + 2 <= 2 N_d  */
     int timing;        /* 1 = record per-stage CUDA events (read back by nufft_get_info)              */
-    int spread_warps;  /* warps per spread CTA (z-plane owners): 4 or 8; 0 = built-in choice          */
+    int spread_warps;  /* spread kernel: 0 = built-in choice; 1 = register rows, 2 = register outer   *
+                        * products (both need T_d = 16 - w); 4 / 8 = smem z-plane owners, that many warps */
     int reserved[6];
 } nufft_opts;
 
@@ -167,6 +168,17 @@ int nufft_pif_kick(nufft_handle h, int64_t Np, void* v, const void* e, double sc
 /* Drift: x += v dt on each axis, folded onto [0, L). */
 int nufft_pif_drift(nufft_handle h, int64_t Np, void* x, void* y, void* z, const void* vx,
                     const void* vy, const void* vz, double dt);
+/* Particle migration for a slab plan created with opts.points_owned = 1 (PAPER.md:229-235:
+ * "particles are partitioned according to the same spatial decomposition" as the grid).
+ * Collective over the plan's ranks.  In: this rank's *np particles (x y z vx vy vz, six
+ * device arrays of capacity cap >= *np).  Every particle whose fine z-cell lies outside
+ * this rank's slab is sent to its owner (NCCL send/recv of the leavers only); the staying
+ * particles are compacted into [0, *np - leavers) in place (their order may change) and
+ * the arrivals appended.  Out: *np = the new local count.  NUFFT_ERR_NPTS on EVERY rank
+ * if the new count of any rank would exceed its cap (agreed collectively before anything
+ * moves: all particles stay where they were).  On a one-GPU plan: no-op. */
+int nufft_pif_migrate(nufft_handle h, int64_t* np, int64_t cap, void* x, void* y, void* z,
+                      void* vx, void* vy, void* vz);
 
 #ifdef __cplusplus
 }

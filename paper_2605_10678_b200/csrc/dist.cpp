@@ -71,6 +71,13 @@ struct DistState {
     void* sbuf = nullptr;  // send staging (3 coords or complex values), np_user elements
     void* rbuf = nullptr;  // receive staging, np_local elements
     size_t sbuf_bytes = 0, rbuf_bytes = 0;
+
+    // PIF particle migration (nufft_pif_migrate)
+    unsigned long long* d_mig = nullptr;  // [P] pack cursors, [2] hole / tail counters, [1] flag
+    void* mig_send = nullptr;             // leavers, 6 values each
+    void* mig_recv = nullptr;             // arrivals, 6 values each
+    void* mig_idx = nullptr;              // 3 nleave int64: vacated slots, holes, tail stayers
+    size_t mig_send_bytes = 0, mig_recv_bytes = 0, mig_idx_bytes = 0;
 };
 
 namespace {
@@ -269,6 +276,7 @@ int dist_init(nufft_plan_s* p) {
     if ((st = dev_alloc(p, (void**)&d->d_counts, sizeof(unsigned long long) * P))) return st;
     if ((st = dev_alloc(p, (void**)&d->d_rcounts, sizeof(unsigned long long) * P))) return st;
     if ((st = dev_alloc(p, (void**)&d->d_off, sizeof(unsigned long long) * P))) return st;
+    if ((st = dev_alloc(p, (void**)&d->d_mig, sizeof(unsigned long long) * (P + 3)))) return st;
     d->scount.assign(P, 0);
     d->soff.assign(P, 0);
     d->rcount.assign(P, 0);
@@ -459,13 +467,103 @@ void dist_destroy(nufft_plan_s* p) {
     dev_free(p, (void**)&d->rank_in, 0);
     dev_free(p, &d->sbuf, 0);
     dev_free(p, &d->rbuf, 0);
+    dev_free(p, (void**)&d->d_mig, 0);
+    dev_free(p, &d->mig_send, 0);
+    dev_free(p, &d->mig_recv, 0);
+    dev_free(p, &d->mig_idx, 0);
     delete d;
     p->dist = nullptr;
+}
+
+// PIF particle migration: particles that drifted out of this rank's slab move to
+// their owner; the rest are compacted in place.  Only the leavers (a small
+// fraction per step) are copied or sent.
+template <typename T>
+int migrate_t(nufft_plan_s* p, int64_t* np, int64_t cap, T* const st[6]) {
+    DistState* d = p->dist;
+    const int P = d->P;
+    const int64_t n = *np;
+    const Geom& g = p->geom;
+    const size_t rs = sizeof(T);
+    NUFFT_CK(cudaMemsetAsync(d->d_counts, 0, sizeof(unsigned long long) * P, p->stream));
+    NUFFT_CK(launch_migrate_count<T>(n, st[2], g.L, g.scale[2], p->nf[2], (int)d->nzl, d->r,
+                                     d->d_counts, p->stream));
+    NCK(ncclAlltoAll(d->d_counts, d->d_rcounts, 1, ncclUint64, d->nccl, p->stream));
+    NUFFT_CK(cudaMemcpyAsync(d->scount.data(), d->d_counts, sizeof(unsigned long long) * P,
+                             cudaMemcpyDeviceToHost, p->stream));
+    NUFFT_CK(cudaMemcpyAsync(d->rcount.data(), d->d_rcounts, sizeof(unsigned long long) * P,
+                             cudaMemcpyDeviceToHost, p->stream));
+    NUFFT_CK(cudaStreamSynchronize(p->stream));
+    unsigned long long so = 0, ro = 0;
+    for (int q = 0; q < P; ++q) {
+        d->soff[q] = so;
+        d->roff[q] = ro;
+        so += d->scount[q];
+        ro += d->rcount[q];
+    }
+    const int64_t nleave = (int64_t)so, nrecv = (int64_t)ro;
+    // every rank must agree before any particle moves: a rank without room fails
+    // the call on ALL ranks (no rank may be left waiting in the exchange)
+    {
+        unsigned long long flag = (n - nleave + nrecv > cap) ? 1ull : 0ull;
+        NUFFT_CK(cudaMemcpyAsync(d->d_mig + P + 2, &flag, sizeof(flag), cudaMemcpyHostToDevice,
+                                 p->stream));
+        NCK(ncclAllReduce(d->d_mig + P + 2, d->d_mig + P + 2, 1, ncclUint64, ncclMax, d->nccl,
+                          p->stream));
+        NUFFT_CK(cudaMemcpyAsync(&flag, d->d_mig + P + 2, sizeof(flag), cudaMemcpyDeviceToHost,
+                                 p->stream));
+        NUFFT_CK(cudaStreamSynchronize(p->stream));
+        if (flag) return NUFFT_ERR_NPTS;  // state untouched on every rank
+    }
+    int s;
+    if ((s = ensure(p, &d->mig_send, &d->mig_send_bytes, 6 * (size_t)nleave * rs + 16))) return s;
+    if ((s = ensure(p, &d->mig_recv, &d->mig_recv_bytes, 6 * (size_t)nrecv * rs + 16))) return s;
+    if ((s = ensure(p, &d->mig_idx, &d->mig_idx_bytes, 3 * (size_t)nleave * 8 + 16))) return s;
+    NUFFT_CK(cudaMemcpyAsync(d->d_off, d->soff.data(), sizeof(unsigned long long) * P,
+                             cudaMemcpyHostToDevice, p->stream));
+    NUFFT_CK(cudaMemsetAsync(d->d_mig, 0, sizeof(unsigned long long) * (P + 2), p->stream));
+    int64_t* idx = static_cast<int64_t*>(d->mig_idx);
+    T* send = static_cast<T*>(d->mig_send);
+    T* recv = static_cast<T*>(d->mig_recv);
+    NUFFT_CK(launch_migrate_move<T>(n, nleave, nrecv, st, g.L, g.scale[2], p->nf[2], (int)d->nzl,
+                                    d->r, d->d_off, d->d_mig, send, recv, idx, idx + nleave,
+                                    idx + 2 * nleave, d->d_mig + P, 0, p->stream));
+    NCK(ncclGroupStart());
+    for (int q = 0; q < P; ++q) {
+        if (d->scount[q])
+            NCK(ncclSend(send + 6 * d->soff[q], 6 * d->scount[q] * rs, ncclChar, q, d->nccl,
+                         p->stream));
+        if (d->rcount[q])
+            NCK(ncclRecv(recv + 6 * d->roff[q], 6 * d->rcount[q] * rs, ncclChar, q, d->nccl,
+                         p->stream));
+    }
+    NCK(ncclGroupEnd());
+    NUFFT_CK(launch_migrate_move<T>(n, nleave, nrecv, st, g.L, g.scale[2], p->nf[2], (int)d->nzl,
+                                    d->r, d->d_off, d->d_mig, send, recv, idx, idx + nleave,
+                                    idx + 2 * nleave, d->d_mig + P, 1, p->stream));
+    *np = n - nleave + nrecv;
+    return NUFFT_OK;
 }
 
 }  // namespace nufft
 
 extern "C" {
+
+int nufft_pif_migrate(nufft_handle p, int64_t* np, int64_t cap, void* x, void* y, void* z,
+                      void* vx, void* vy, void* vz) {
+    if (!p || !np || *np < 0 || cap < *np) return NUFFT_ERR_ARG;
+    if (!p->dist) return NUFFT_OK;  // one GPU: every particle is local
+    if (*np > 0 && (!x || !y || !z || !vx || !vy || !vz)) return NUFFT_ERR_ARG;
+    cudaGetLastError();
+    if (p->prec == NUFFT_F64) {
+        double* st[6] = {static_cast<double*>(x), static_cast<double*>(y), static_cast<double*>(z),
+                         static_cast<double*>(vx), static_cast<double*>(vy), static_cast<double*>(vz)};
+        return nufft::migrate_t<double>(p, np, cap, st);
+    }
+    float* st[6] = {static_cast<float*>(x), static_cast<float*>(y), static_cast<float*>(z),
+                    static_cast<float*>(vx), static_cast<float*>(vy), static_cast<float*>(vz)};
+    return nufft::migrate_t<float>(p, np, cap, st);
+}
 
 int nufft_comm_unique_id(char id[128]) {
     if (!id) return NUFFT_ERR_ARG;

@@ -183,6 +183,112 @@ __global__ void xy_unpad_kernel(const C* __restrict__ recv, int64_t nf1, int64_t
     }
 }
 
+// ---------------------------------------------------------------- PIF particle migration
+// A particle's owner is the z-slab of its fine cell (the owner_count rule).
+template <typename T>
+__device__ __forceinline__ uint32_t slab_owner(T z, double L, double scale, int64_t nf3, int nzl) {
+    const double s = fold_rescale_d((double)z, L, scale, nf3);
+    int64_t c = (int64_t)s;
+    if (c >= nf3) c = nf3 - 1;
+    return (uint32_t)(c / nzl);
+}
+
+// pass 1: per-destination counts of the particles that left this rank's slab
+template <typename T>
+__global__ void migrate_count_kernel(int64_t n, const T* __restrict__ z, double L, double scale,
+                                     int64_t nf3, int nzl, uint32_t me,
+                                     unsigned long long* __restrict__ counts) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i - lane < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t o = me;
+        if (i < n) o = slab_owner(z[i], L, scale, nf3, nzl);
+        const bool leave = o != me;
+        const unsigned act = __ballot_sync(0xffffffffu, leave);
+        if (leave) {
+            const unsigned peers = __match_any_sync(act, o);
+            if (lane == __ffs(peers) - 1) atomicAdd(&counts[o], (unsigned long long)__popc(peers));
+        }
+    }
+}
+
+// pass 2: leavers -> send records (6 values: x y z vx vy vz), grouped by
+// destination; hole[pos] = the slot they vacate
+template <typename T>
+__global__ void migrate_pack_kernel(int64_t n, const T* __restrict__ x, const T* __restrict__ y,
+                                    const T* __restrict__ z, const T* __restrict__ vx,
+                                    const T* __restrict__ vy, const T* __restrict__ vz, double L,
+                                    double scale, int64_t nf3, int nzl, uint32_t me,
+                                    const unsigned long long* __restrict__ off,
+                                    unsigned long long* __restrict__ cursor, T* __restrict__ send,
+                                    int64_t* __restrict__ hole) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i - lane < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t o = me;
+        if (i < n) o = slab_owner(z[i], L, scale, nf3, nzl);
+        const bool leave = o != me;
+        const unsigned act = __ballot_sync(0xffffffffu, leave);
+        if (leave) {
+            const unsigned peers = __match_any_sync(act, o);
+            const int leader = __ffs(peers) - 1;
+            unsigned long long base = 0;
+            if (lane == leader) base = atomicAdd(&cursor[o], (unsigned long long)__popc(peers));
+            base = __shfl_sync(peers, base, leader);
+            const int64_t pos = (int64_t)(off[o] + base + __popc(peers & ((1u << lane) - 1u)));
+            T* r = send + 6 * pos;
+            r[0] = x[i]; r[1] = y[i]; r[2] = z[i]; r[3] = vx[i]; r[4] = vy[i]; r[5] = vz[i];
+            hole[pos] = i;
+        }
+    }
+}
+
+// pass 3: the vacated slots below the new count ...
+__global__ void migrate_holes_kernel(int64_t nleave, const int64_t* __restrict__ hole,
+                                     int64_t new_n, int64_t* __restrict__ lo,
+                                     unsigned long long* __restrict__ nlo) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nleave;
+         k += (int64_t)gridDim.x * blockDim.x)
+        if (hole[k] < new_n) lo[atomicAdd(nlo, 1ull)] = hole[k];
+}
+
+// ... and the staying particles at or above it (as many as there are such holes)
+template <typename T>
+__global__ void migrate_tail_kernel(int64_t n, int64_t new_n, const T* __restrict__ z, double L,
+                                    double scale, int64_t nf3, int nzl, uint32_t me,
+                                    int64_t* __restrict__ tail,
+                                    unsigned long long* __restrict__ ntail) {
+    for (int64_t i = new_n + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        if (slab_owner(z[i], L, scale, nf3, nzl) == me) tail[atomicAdd(ntail, 1ull)] = i;
+}
+
+// pass 4: tail particles fill the holes (state arrays compacted to [0, new_n))
+template <typename T>
+__global__ void migrate_fill_kernel(const unsigned long long* __restrict__ nholes,
+                                    const int64_t* __restrict__ lo,
+                                    const int64_t* __restrict__ tail, T* x, T* y, T* z, T* vx,
+                                    T* vy, T* vz) {
+    const int64_t h = (int64_t)*nholes;  // == number of tail stayers (pass 3)
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < h;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t d = lo[k], s = tail[k];
+        x[d] = x[s]; y[d] = y[s]; z[d] = z[s]; vx[d] = vx[s]; vy[d] = vy[s]; vz[d] = vz[s];
+    }
+}
+
+// pass 5: received records appended at [new_n, new_n + nrecv)
+template <typename T>
+__global__ void migrate_unpack_kernel(int64_t nrecv, const T* __restrict__ recv, int64_t at, T* x,
+                                      T* y, T* z, T* vx, T* vy, T* vz) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nrecv;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const T* r = recv + 6 * k;
+        x[at + k] = r[0]; y[at + k] = r[1]; z[at + k] = r[2];
+        vx[at + k] = r[3]; vy[at + k] = r[4]; vz[at + k] = r[5];
+    }
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------- launchers
@@ -262,6 +368,44 @@ cudaError_t launch_xy_unpad(const typename Cx<T>::type* recv, const int64_t nf[3
     return cudaGetLastError();
 }
 
+template <typename T>
+cudaError_t launch_migrate_count(int64_t n, const T* z, double L, double scale, int64_t nf3,
+                                 int nzl, int me, unsigned long long* counts, cudaStream_t s) {
+    if (n > 0)
+        migrate_count_kernel<T><<<grid1d(n), kThreads, 0, s>>>(n, z, L, scale, nf3, nzl,
+                                                               (uint32_t)me, counts);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_migrate_move(int64_t n, int64_t nleave, int64_t nrecv, T* const st[6],
+                                double L, double scale, int64_t nf3, int nzl, int me,
+                                const unsigned long long* off, unsigned long long* cursor,
+                                T* send, const T* recv, int64_t* hole, int64_t* lo,
+                                int64_t* tail, unsigned long long* nlo_ntail, int phase,
+                                cudaStream_t s) {
+    const int64_t new_n = n - nleave;
+    if (phase == 0) {  // pack leavers, list holes and tail stayers, fill the holes
+        if (nleave > 0) {
+            migrate_pack_kernel<T><<<grid1d(n), kThreads, 0, s>>>(
+                n, st[0], st[1], st[2], st[3], st[4], st[5], L, scale, nf3, nzl, (uint32_t)me,
+                off, cursor, send, hole);
+            migrate_holes_kernel<<<grid1d(nleave), kThreads, 0, s>>>(nleave, hole, new_n, lo,
+                                                                     nlo_ntail);
+            migrate_tail_kernel<T><<<grid1d(nleave), kThreads, 0, s>>>(
+                n, new_n, st[2], L, scale, nf3, nzl, (uint32_t)me, tail, nlo_ntail + 1);
+            // holes below new_n == stayers at or above it (both counted on the device;
+            // nleave bounds them)
+            migrate_fill_kernel<T><<<grid1d(nleave), kThreads, 0, s>>>(
+                nlo_ntail, lo, tail, st[0], st[1], st[2], st[3], st[4], st[5]);
+        }
+    } else if (nrecv > 0) {
+        migrate_unpack_kernel<T><<<grid1d(nrecv), kThreads, 0, s>>>(
+            nrecv, recv, new_n, st[0], st[1], st[2], st[3], st[4], st[5]);
+    }
+    return cudaGetLastError();
+}
+
 #define NUFFT_DIST_INST(T)                                                                         \
     template cudaError_t launch_owner_count<T>(int64_t, const T*, double, double, int64_t, int,      \
                                                uint32_t*, uint32_t*, unsigned long long*,            \
@@ -280,6 +424,20 @@ cudaError_t launch_xy_unpad(const typename Cx<T>::type* recv, const int64_t nf[3
                                             const int64_t*, int, int, Cx<T>::type*, cudaStream_t);
 NUFFT_DIST_INST(float)
 NUFFT_DIST_INST(double)
+template cudaError_t launch_migrate_count<float>(int64_t, const float*, double, double, int64_t,
+                                                 int, int, unsigned long long*, cudaStream_t);
+template cudaError_t launch_migrate_count<double>(int64_t, const double*, double, double, int64_t,
+                                                  int, int, unsigned long long*, cudaStream_t);
+template cudaError_t launch_migrate_move<float>(int64_t, int64_t, int64_t, float* const*, double,
+                                                double, int64_t, int, int,
+                                                const unsigned long long*, unsigned long long*,
+                                                float*, const float*, int64_t*, int64_t*,
+                                                int64_t*, unsigned long long*, int, cudaStream_t);
+template cudaError_t launch_migrate_move<double>(int64_t, int64_t, int64_t, double* const*, double,
+                                                 double, int64_t, int, int,
+                                                 const unsigned long long*, unsigned long long*,
+                                                 double*, const double*, int64_t*, int64_t*,
+                                                 int64_t*, unsigned long long*, int, cudaStream_t);
 #undef NUFFT_DIST_INST
 
 }  // namespace nufft

@@ -140,6 +140,20 @@ template <typename T>
 cudaError_t launch_owner_count(int64_t Np, const T* z, double L, double scale, int64_t nf3,
                                int nzl, uint32_t* owner, uint32_t* rank_in,
                                unsigned long long* counts, cudaStream_t s);
+// PIF particle migration (nufft_pif_migrate): per-destination counts of the
+// particles outside this rank's slab; then phase 0 = pack leavers into `send`
+// (6 values each, grouped by destination at `off`), compact the staying ones into
+// [0, n - nleave); phase 1 = append the nrecv received records there
+template <typename T>
+cudaError_t launch_migrate_count(int64_t n, const T* z, double L, double scale, int64_t nf3,
+                                 int nzl, int me, unsigned long long* counts, cudaStream_t s);
+template <typename T>
+cudaError_t launch_migrate_move(int64_t n, int64_t nleave, int64_t nrecv, T* const st[6],
+                                double L, double scale, int64_t nf3, int nzl, int me,
+                                const unsigned long long* off, unsigned long long* cursor,
+                                T* send, const T* recv, int64_t* hole, int64_t* lo,
+                                int64_t* tail, unsigned long long* nlo_ntail, int phase,
+                                cudaStream_t s);
 cudaError_t launch_pack_bytes(int64_t Np, int elem_bytes, const void* src, const uint32_t* owner,
                               const uint32_t* rank_in, const unsigned long long* off, void* dst,
                               bool unpack, cudaStream_t s);

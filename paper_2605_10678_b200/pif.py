@@ -9,10 +9,12 @@ Plasma units, electrons q/m = -1, total charge Q_e = -L^3, L = 2 pi / k
 arithmetic step runs in libnufft kernels (type 1/2, nufft_pif_poisson,
 nufft_pif_kick, nufft_pif_drift); this class holds buffers and calls them.
 
-With a Comm the plan is a z-slab plan: each rank samples ITS slab's share of
-the Landau distribution (z conditioned on the slab), points keep being owned by
-the rank that created them, and setpts moves only the ones that crossed a slab
-boundary to their current owner for the transforms (results come back).
+With a Comm the plan is a z-slab plan (particles partitioned
+like the grid): each rank samples ITS slab's share of the Landau distribution (z
+conditioned on the slab) and OWNS the particles in its slab (opts.points_owned).
+After every drift, nufft_pif_migrate sends the few particles that crossed a slab
+boundary, with their velocities, to the new owner -- the transforms themselves
+never move points.  Particle arrays carry slack capacity for the migration.
 """
 from __future__ import annotations
 
@@ -33,7 +35,7 @@ class LandauPIF:
         self.L = 2 * math.pi / k
         self.qm = -1.0
         self.plan = _n.Plan(N, eps, precision=precision, L=self.L, comm=comm, device=device,
-                            timing=timing)
+                            timing=timing, points_owned=comm is not None)
         dev = self.plan.device
         rdt, cdt = self.plan.real, self.plan.cplx
         self.Np_total = int(Np)
@@ -51,34 +53,68 @@ class LandauPIF:
             assert nf3 % P == 0 and f1 > f0
             pts = synthetic.landau_points(self.Np, alpha=alpha, k=k, seed=seed + 7919 * r,
                                           device=dev, dtype=rdt, z_range=(z0, z1))
-        self.x, self.y, self.z = (p.contiguous() for p in pts)
         vel = synthetic.maxwellian_velocities(self.Np, seed=seed + 4 + 104729 * (comm.rank if comm else 0),
                                               device=dev, dtype=rdt)
-        self.vx, self.vy, self.vz = (v.contiguous() for v in vel)
+        # particle state with slack capacity (slab plans: migration changes the count)
+        self.cap = self.Np if comm is None else self.Np + self.Np // 8 + 4096
+        src = [*pts, *vel]
+        del pts, vel
+        self._state = []
+        while src:                                          # one array at a time (memory)
+            a = src.pop(0)
+            if self.cap == self.Np:
+                self._state.append(a.contiguous())
+            else:
+                buf = torch.empty(self.cap, dtype=rdt, device=dev)
+                buf[:self.Np].copy_(a)
+                self._state.append(buf)
+            del a
         self.q = -self.L ** 3 / self.Np_total              # Q_e = -L^3 shared equally
-        self.charge = torch.full((self.Np,), self.q, dtype=cdt, device=dev)
+        self.charge = torch.full((self.cap,), self.q, dtype=cdt, device=dev)
         shape = self.plan.local_shape
         self.rho_k = torch.empty(shape, dtype=cdt, device=dev)
         self.e_k = [torch.empty(shape, dtype=cdt, device=dev) for _ in range(3)]
-        self.e_pts = torch.empty(self.Np, dtype=cdt, device=dev)
+        self.e_pts = torch.empty(self.cap, dtype=cdt, device=dev)
         self.t = 0.0
+        if comm is not None:
+            self.migrate()   # sampling at a slab edge may round into the neighbour's cell
+
+    # views of this rank's particles
+    x = property(lambda s: s._state[0][:s.Np])
+    y = property(lambda s: s._state[1][:s.Np])
+    z = property(lambda s: s._state[2][:s.Np])
+    vx = property(lambda s: s._state[3][:s.Np])
+    vy = property(lambda s: s._state[4][:s.Np])
+    vz = property(lambda s: s._state[5][:s.Np])
+
+    def migrate(self):
+        """Hand particles that left this rank's slab to their owners (collective)."""
+        n = ctypes.c_int64(self.Np)
+        _n._check(_n.lib().nufft_pif_migrate(self.plan._h, ctypes.byref(n), self.cap,
+                                             *(ctypes.c_void_p(a.data_ptr()) for a in self._state)),
+                  "nufft_pif_migrate")
+        self.Np = int(n.value)
 
     def step(self):
         p, L = self.plan, _n.lib()
+        n = self.Np
         with torch.cuda.device(p.device):
             p.setpts(self.x, self.y, self.z)                                   # sort
-            p.type1(self.charge, out=self.rho_k)                               # (1) scatter
+            p.type1(self.charge[:n], out=self.rho_k)                           # (1) scatter
             _n._check(L.nufft_pif_poisson(p._h, self.rho_k.data_ptr(), *(e.data_ptr() for e in self.e_k)),
                       "nufft_pif_poisson")                                      # (2) field solve
             s = self.qm * self.dt / self.L ** 3
+            e_pts = self.e_pts[:n]
             for e_k, v in zip(self.e_k, (self.vx, self.vy, self.vz)):
-                p.type2(e_k, out=self.e_pts)                                    # (3) gather
-                _n._check(L.nufft_pif_kick(p._h, self.Np, ctypes.c_void_p(v.data_ptr()),
-                                           ctypes.c_void_p(self.e_pts.data_ptr()), ctypes.c_double(s)),
+                p.type2(e_k, out=e_pts)                                         # (3) gather
+                _n._check(L.nufft_pif_kick(p._h, n, ctypes.c_void_p(v.data_ptr()),
+                                           ctypes.c_void_p(e_pts.data_ptr()), ctypes.c_double(s)),
                           "nufft_pif_kick")                                     # (4) push
-            _n._check(L.nufft_pif_drift(p._h, self.Np, *(ctypes.c_void_p(a.data_ptr()) for a in
-                                                         (self.x, self.y, self.z, self.vx, self.vy, self.vz)),
+            _n._check(L.nufft_pif_drift(p._h, n, *(ctypes.c_void_p(a.data_ptr()) for a in
+                                                   (self.x, self.y, self.z, self.vx, self.vy, self.vz)),
                                         ctypes.c_double(self.dt)), "nufft_pif_drift")
+            if p.comm is not None:
+                self.migrate()                                                  # slab ownership
         self.t += self.dt
 
     def field_energy(self) -> float:
