@@ -166,8 +166,13 @@ __device__ __forceinline__ void produce(int tid, const PtsView<T>& p,
     }
 }
 
+// resident CTAs per SM: fp64 needs 128 registers (2 CTAs); fp32 fits 3 (<= 85
+// registers, 3 x 71 KB shared memory), which hides the per-bin prologue latency
+// at low density (one batch per bin)
+template <typename T> struct OuterMinBlocks { static constexpr int value = sizeof(T) == 4 ? 3 : 2; };
+
 template <typename T, int W>
-__global__ void __launch_bounds__(kOutThreads, 2)
+__global__ void __launch_bounds__(kOutThreads, OuterMinBlocks<T>::value)
     spread_outer_kernel(Geom g, PtsView<T> p, const typename Cx<T>::type* __restrict__ c,
                         typename Cx<T>::type* __restrict__ grid, T beta) {
     using C = typename Cx<T>::type;
