@@ -75,7 +75,10 @@ typedef struct {
     int timing;        /* 1 = record per-stage CUDA events (read back by nufft_get_info)              */
     int spread_warps;  /* spread kernel: 0 = built-in choice; 1 = register rows, 2 = register outer   *
                         * products (both need T_d = 16 - w); 4 / 8 = smem z-plane owners, that many warps */
-    int reserved[6];
+    int precompute;    /* ES weights of every point (3 w reals, sorted order) computed once by setpts and
+                        * read by every execute / spread / interp instead of re-evaluating phi:
+                        * 0 = auto (when they fit in 1/4 of the device memory), 1 = always, -1 = never */
+    int reserved[5];
 } nufft_opts;
 
 typedef struct {
@@ -93,6 +96,7 @@ typedef struct {
     int64_t slab_lo, slab_hi; /* fine z-planes owned by this rank                     */
     /* per-stage device milliseconds of the most recent calls (opts.timing = 1), else -1 */
     float ms_setpts, ms_spread, ms_fold, ms_fft, ms_deconv, ms_pad, ms_interp, ms_comm;
+    int weights_precomputed; /* 1 if the last setpts stored the per-point ES weights     */
 } nufft_info;
 
 /* Fills *o with the defaults (L = 2 pi, centered modes, default stream, single GPU). */

@@ -27,6 +27,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
           "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 CU_FLAGS = ARCH + COMMON + ["--expt-relaxed-constexpr", "-Xptxas", "-v"]
+# developer instrumentation only (e.g. -DNUFFT_OUTER_PROF); never set for the product build
+CU_FLAGS += os.environ.get("NUFFT_EXTRA_NVCC_FLAGS", "").split()
 
 SOURCES = ["sort.cu", "spread.cu", "spread_rows.cu", "spread_outer.cu", "interp.cu",
            "elementwise.cu", "pif.cu", "dist_kernels.cu", "plan.cpp", "dist.cpp"]

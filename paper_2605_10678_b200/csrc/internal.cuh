@@ -65,6 +65,8 @@ static_assert(sizeof(PtRec<double>) == 32 && sizeof(PtRec<float>) == 32, "one se
 template <typename T> struct PtsView {
     const uint32_t* offset;  // nbins + 1 bin starts (exclusive scan of counts)
     const PtRec<T>* rec;     // Np sorted records
+    const T* w;              // Np x 3w ES weights in sorted order ([x | y | z] per point,
+                             // node k of axis d at 3w i + w d + k), or nullptr: evaluate phi
 };
 
 // ---------------------------------------------------------------- kernel launchers
@@ -75,6 +77,10 @@ cudaError_t launch_bin_sort(const Geom& g, int64_t Np, const T* x, const T* y, c
                             uint32_t* bin_of, uint32_t* rank_of, PtRec<T>* rec, int64_t nbins,
                             cudaStream_t s);
 size_t scan_blocksum_elems(int64_t nbins);
+// setpts (precompute): w[3w i + w d + k] = phi(2 (k - rec[i].d[d]) / w)
+template <typename T>
+cudaError_t launch_weights(const PtRec<T>* rec, int64_t Np, int w, double beta, T* out,
+                           cudaStream_t s);
 
 // spread.cu: grid (nf[0] x nf[1] x nz_loc complex, x fastest) += C c
 template <typename T>

@@ -130,12 +130,22 @@ __global__ void __launch_bounds__(kInterpThreads, 2)
             my_perm = rr.perm;
             my_base = (int)(((la >> 16) * Ey + ((la >> 8) & 0xff)) * pitch + (la & 0xff)) +
                       tx.shift;
-            T* wl = wb + lane * WS;
+            if (!p.w) {
+                T* wl = wb + lane * WS;
 #pragma unroll
-            for (int d = 0; d < 3; ++d)
+                for (int d = 0; d < 3; ++d)
 #pragma unroll
-                for (int k = 0; k < W; ++k)
-                    wl[d * W + k] = es_weight<T>(((T)k - d3[d]) * two_over_w, beta);
+                    for (int k = 0; k < W; ++k)
+                        wl[d * W + k] = es_weight<T>(((T)k - d3[d]) * two_over_w, beta);
+            }
+        }
+        if (p.w) {  // precomputed at setpts: the chunk's rows are contiguous, copy coalesced
+            const T* src = p.w + (size_t)c0 * (3 * W);
+            const int ne = (int)min(32u, wend - c0) * (3 * W);
+            for (int e = lane; e < ne; e += 32) {
+                const int j = e / (3 * W);
+                wb[j * WS + (e - j * (3 * W))] = src[e];
+            }
         }
         if (!staged) {
             mbar_wait(bar, 0);

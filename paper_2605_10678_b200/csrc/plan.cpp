@@ -158,6 +158,7 @@ PtsView<T> pts_view(nufft_plan_s* p) {
     PtsView<T> v;
     v.offset = p->offset;
     v.rec = static_cast<const PtRec<T>*>(p->rec);
+    v.w = p->wts_on ? static_cast<const T*>(p->wts) : nullptr;
     return v;
 }
 
@@ -193,6 +194,44 @@ int local_sort(nufft_plan_s* p, int64_t Np, const void* xd, const void* yd, cons
                                         p->blocksum, p->bin_of, p->rank_of,
                                         static_cast<PtRec<float>*>(p->rec), p->nbins, p->stream));
     p->Np = Np;
+    // per-point ES weights, reused by every execute on these points
+    p->wts_on = false;
+    if (p->precompute >= 0 && Np > 0) {
+        const size_t need = (size_t)Np * 3 * (size_t)p->w * p->real_size;
+        bool want = p->precompute > 0 || p->wts_bytes >= need;  // no query when it fits
+        if (!want) {  // auto: when the table fits in a quarter of the device memory
+            // (cudaMemGetInfo synchronises: asked only when a (re)allocation is needed)
+            size_t fr = 0, tot = 0;
+            if (cudaMemGetInfo(&fr, &tot) == cudaSuccess)
+                want = need <= tot / 4 && (p->wts_bytes >= need || need + (64u << 20) < fr);
+            else
+                cudaGetLastError();
+        }
+        if (want) {
+            if (p->wts_bytes < need) {
+                dev_free(p, &p->wts, p->wts_bytes);
+                p->wts_bytes = 0;
+                const size_t n = p->dist ? need + need / 16 : need;
+                if ((st = dev_alloc(p, &p->wts, n))) {
+                    if (p->precompute > 0) return st;
+                    st = NUFFT_OK;  // auto: fall back to evaluating phi in the kernels
+                } else {
+                    p->wts_bytes = n;
+                }
+            }
+            if (p->wts_bytes >= need) {
+                if (p->prec == NUFFT_F64)
+                    NUFFT_CK(launch_weights<double>(static_cast<const PtRec<double>*>(p->rec), Np,
+                                                    p->w, p->beta, static_cast<double*>(p->wts),
+                                                    p->stream));
+                else
+                    NUFFT_CK(launch_weights<float>(static_cast<const PtRec<float>*>(p->rec), Np,
+                                                   p->w, p->beta, static_cast<float*>(p->wts),
+                                                   p->stream));
+                p->wts_on = true;
+            }
+        }
+    }
     return NUFFT_OK;
 }
 
@@ -333,6 +372,11 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
     p->timing = o.timing != 0;
     p->comm = o.comm;
     p->points_owned = o.points_owned;
+    if (o.precompute < -1 || o.precompute > 1) {
+        delete p;
+        return NUFFT_ERR_ARG;
+    }
+    p->precompute = o.precompute;
 
     Geom& g = p->geom;
     for (int d = 0; d < 3; ++d) {
@@ -576,6 +620,7 @@ int nufft_destroy(nufft_handle p) {
     dev_free(p, (void**)&p->bin_of, 0);
     dev_free(p, (void**)&p->rank_of, 0);
     dev_free(p, &p->rec, 0);
+    dev_free(p, &p->wts, 0);
     dev_free(p, &p->stage_in, 0);
     dev_free(p, &p->stage_out, 0);
     if (p->timing)
@@ -626,6 +671,7 @@ int nufft_get_info(nufft_handle p, nufft_info* info) {
     info->ms_pad = ms[EV_PAD];
     info->ms_interp = ms[EV_INTERP];
     info->ms_comm = ms[EV_COMM];
+    info->weights_precomputed = p->wts_on ? 1 : 0;
     return NUFFT_OK;
 }
 

@@ -46,6 +46,11 @@ struct nufft_plan_s {
     uint32_t* bin_of = nullptr;
     uint32_t* rank_of = nullptr;
     void* rec = nullptr;  // Np sorted 32-byte records (PtRec)
+    // per-point ES weights (opts.precompute): Np x 3w reals in sorted order
+    int precompute = 0;     // opts value: 0 auto, 1 always, -1 never
+    void* wts = nullptr;
+    size_t wts_bytes = 0;
+    bool wts_on = false;    // the last setpts filled wts
 
     // host staging
     void* stage_in = nullptr;

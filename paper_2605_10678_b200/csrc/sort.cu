@@ -15,6 +15,7 @@
 //   k3 scatter   : slot = offset[bin] + rank; the sorted 32-byte stencil record
 //                  (phase offsets d, local base la, caller index) is written
 //                  to the slot as one full DRAM sector.
+#include "device_util.cuh"
 #include "internal.cuh"
 
 namespace nufft {
@@ -243,6 +244,39 @@ __global__ void __launch_bounds__(kSortThreads) scatter_kernel(
     }
 }
 
+// Per-point ES weights in sorted order (opts.precompute): one thread per point
+// evaluates its 3w weights (3w independent evaluations: no dependent chain) and
+// stages them in shared memory; the block then writes its points' rows as one
+// contiguous, coalesced run.
+constexpr int kWThreads = 128;  // 128 x 3w x 8 B <= 48 KB of static shared memory
+
+template <typename T, int W>
+__global__ void __launch_bounds__(kWThreads) weights_kernel(const PtRec<T>* __restrict__ rec,
+                                                             int64_t Np, T beta,
+                                                             T* __restrict__ out) {
+    constexpr int R = 3 * W;
+    __shared__ T stage[kWThreads * R];
+    const T two_over_w = (T)2 / (T)W;
+    for (int64_t base = (int64_t)blockIdx.x * kWThreads; base < Np;
+         base += (int64_t)gridDim.x * kWThreads) {
+        const int64_t i = base + threadIdx.x;
+        if (i < Np) {
+            const PtRec<T> r = rec[i];
+#pragma unroll
+            for (int d = 0; d < 3; ++d)
+#pragma unroll
+                for (int k = 0; k < W; ++k)
+                    stage[threadIdx.x * R + d * W + k] =
+                        dev::es_weight<T>(((T)k - r.d[d]) * two_over_w, beta);
+        }
+        __syncthreads();
+        const int64_t n = min((int64_t)kWThreads, Np - base);
+        T* dst = out + base * R;
+        for (int e = threadIdx.x; e < (int)(n * R); e += kWThreads) dst[e] = stage[e];
+        __syncthreads();
+    }
+}
+
 inline int grid_for(int64_t n, int threads) {
     int64_t b = (n + threads - 1) / threads;
     const int64_t cap = 148 * 16;  // persistent-style cap: 16 resident CTAs per SM
@@ -275,6 +309,31 @@ cudaError_t launch_bin_sort(const Geom& g, int64_t Np, const T* x, const T* y, c
     }
     return cudaGetLastError();
 }
+
+template <typename T>
+cudaError_t launch_weights(const PtRec<T>* rec, int64_t Np, int w, double beta, T* out,
+                           cudaStream_t s) {
+    if (Np <= 0) return cudaSuccess;
+    int64_t blocks = (Np + kWThreads - 1) / kWThreads;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    switch (w) {
+#define NUFFT_WK(WW)                                                                       \
+    case WW:                                                                               \
+        weights_kernel<T, WW><<<(unsigned)blocks, kWThreads, 0, s>>>(rec, Np, (T)beta, out); \
+        break;
+        NUFFT_WK(2) NUFFT_WK(3) NUFFT_WK(4) NUFFT_WK(5) NUFFT_WK(6) NUFFT_WK(7) NUFFT_WK(8)
+        NUFFT_WK(9) NUFFT_WK(10) NUFFT_WK(11) NUFFT_WK(12) NUFFT_WK(13) NUFFT_WK(14)
+        NUFFT_WK(15) NUFFT_WK(16)
+#undef NUFFT_WK
+        default:
+            return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+template cudaError_t launch_weights<float>(const PtRec<float>*, int64_t, int, double, float*,
+                                           cudaStream_t);
+template cudaError_t launch_weights<double>(const PtRec<double>*, int64_t, int, double, double*,
+                                            cudaStream_t);
 
 template cudaError_t launch_bin_sort<float>(const Geom&, int64_t, const float*, const float*,
                                             const float*, uint32_t*, uint32_t*, uint32_t*,

@@ -104,7 +104,8 @@ __global__ void __launch_bounds__(32 * NW)
             const int t = e / W, k = e - t * W;
             const int i = t / 3, d = t - 3 * i;
             const PtRec<T>& rr = p.rec[p0 + i];
-            sw1d[e] = es_weight<T>(((T)k - rr.d[d]) * two_over_w, beta);
+            sw1d[e] = p.w ? p.w[(size_t)p0 * (3 * W) + e]  // precomputed at setpts
+                          : es_weight<T>(((T)k - rr.d[d]) * two_over_w, beta);
             if (d == 2 && k == 0) {
                 const uint32_t la = rr.la;
                 const int lz = (int)(la >> 16);

@@ -84,6 +84,18 @@ template <> struct Vec4<double> {
     }
 };
 
+#ifdef NUFFT_OUTER_PROF
+// debug builds only (-DNUFFT_OUTER_PROF): per warp, clock cycles spent producing,
+// consuming and waiting at the batch barrier, summed over all CTAs
+__device__ unsigned long long g_outer_prof[8][8];  // [warp][produce, consume, barrier, p.zero, p.load, p.scan, p.weights, -]
+#define OUTER_PROF_T(v) const long long v = clock64()
+#define OUTER_PROF_ADD(w, k, d) \
+    if ((threadIdx.x & 31) == 0) atomicAdd(&g_outer_prof[w][k], (unsigned long long)(d))
+#else
+#define OUTER_PROF_T(v)
+#define OUTER_PROF_ADD(w, k, d)
+#endif
+
 template <int BAR, int NT>
 __device__ __forceinline__ void group_sync() {
     if constexpr (BAR == 0) __syncthreads();
@@ -114,11 +126,13 @@ __device__ __forceinline__ void produce(int tid, const PtsView<T>& p,
     constexpr int E = kOutE, B = S::B, TT = E - W, NK = 3 * (TT + 1);
     C* sb = reinterpret_cast<C*>(buf);
     T* swy = reinterpret_cast<T*>(sb + B * E);
+    OUTER_PROF_T(q0);
     // zero the profiles (every row is written densely below only on its stencil)
     float4* z4 = reinterpret_cast<float4*>(buf);
     for (int i = tid; i < (int)(S::buf_bytes / 16); i += NT) z4[i] = float4{0.f, 0.f, 0.f, 0.f};
     for (int i = tid; i < NK; i += NT) m.gcnt[i] = 0;
     group_sync<BAR, NT>();
+    OUTER_PROF_T(q1);
     for (int t = tid; t < n; t += NT) {
         const PtRec<T> r = p.rec[p0 + t];
         const int la = (int)r.la;
@@ -134,6 +148,7 @@ __device__ __forceinline__ void produce(int tid, const PtsView<T>& p,
         m.srank[t] = atomicAdd(&m.gcnt[key], 1);
     }
     group_sync<BAR, NT>();
+    OUTER_PROF_T(q2);
     if (tid < 32) {  // exclusive scan of the NK <= 45 key counts, 2 per lane
         const int lane = tid;
         const int a0 = 2 * lane < NK ? m.gcnt[2 * lane] : 0;
@@ -149,21 +164,43 @@ __device__ __forceinline__ void produce(int tid, const PtsView<T>& p,
         if (2 * lane + 1 <= NK) goff[2 * lane + 1] = ex + a0;
     }
     group_sync<BAR, NT>();
-    // dense weights: one (point, axis, node) per thread
+    OUTER_PROF_T(q3);
+    // weights: one (point, axis) per thread, its w nodes as w independent
+    // evaluations (the producer warps are latency-bound on one dependent
+    // sqrt / exp chain per thread otherwise: measured, scripts/outer_prof.py)
     const T two_over_w = (T)2 / (T)W;
-    for (int e = tid; e < n * 3 * W; e += NT) {
-        const int t = e / (3 * W), r3 = e - t * (3 * W), d = r3 / W, k = r3 - d * W;
+    for (int e = tid; e < n * 3; e += NT) {
+        const int t = e / 3, d = e - 3 * t;
         const int la = m.sla[t];
         const int pos = goff[m.skey[t]] + m.srank[t];
-        const int x = ((la >> (8 * d)) & 0xff) + k;
-        const T wk = es_weight<T>(((T)k - m.sd[4 * t + d]) * two_over_w, beta);
+        const int x0 = (la >> (8 * d)) & 0xff;
+        const T dd = m.sd[4 * t + d];
+        T wk[W];
+#pragma unroll
+        for (int k = 0; k < W; ++k)
+            wk[k] = p.w ? p.w[(size_t)(p0 + t) * (3 * W) + d * W + k]  // precomputed at setpts
+                        : es_weight<T>(((T)k - dd) * two_over_w, beta);
         if (d == 0) {
             const C cv = m.sc[t];
-            sb[pos * E + x] = C{cv.x * wk, cv.y * wk};
+            C* row = sb + pos * E + x0;
+#pragma unroll
+            for (int k = 0; k < W; ++k) row[k] = C{cv.x * wk[k], cv.y * wk[k]};
         } else {
-            swy[(d - 1) * B * E + pos * E + x] = wk;  // d = 1: wy, d = 2: wz
+            T* row = swy + (d - 1) * B * E + pos * E + x0;  // d = 1: wy, d = 2: wz
+#pragma unroll
+            for (int k = 0; k < W; ++k) row[k] = wk[k];
         }
     }
+#ifdef NUFFT_OUTER_PROF
+    if (BAR == 1) {
+        OUTER_PROF_T(q4);
+        const int wp = threadIdx.x >> 5;
+        OUTER_PROF_ADD(wp, 3, q1 - q0);
+        OUTER_PROF_ADD(wp, 4, q2 - q1);
+        OUTER_PROF_ADD(wp, 5, q3 - q2);
+        OUTER_PROF_ADD(wp, 6, q4 - q3);
+    }
+#endif
 }
 
 // resident CTAs per SM: fp64 needs 128 registers (2 CTAs); fp32 fits 3 (<= 85
@@ -184,6 +221,7 @@ __global__ void __launch_bounds__(kOutThreads, OuterMinBlocks<T>::value)
     static_assert(3 * (TT + 1) <= kMaxKeys, "sort keys");
     extern __shared__ __align__(16) unsigned char smem[];
 
+    OUTER_PROF_T(tk0);
     const int b = blockIdx.x;
     const uint32_t beg = p.offset[b], end = p.offset[b + 1];
     if (beg == end) return;
@@ -223,12 +261,14 @@ __global__ void __launch_bounds__(kOutThreads, OuterMinBlocks<T>::value)
                                   reinterpret_cast<T*>(smem), goff0, m, beta);
     __syncthreads();
     for (int kb = 0; kb < nbatch; ++kb) {
+        OUTER_PROF_T(t0);
         if (producer && kb + 1 < nbatch) {
             const uint32_t p1 = beg + (uint32_t)(kb + 1) * B;
             produce<T, W, kProducers, 1>(ptid, p, c, p1, (int)min((uint32_t)B, end - p1),
                                          reinterpret_cast<T*>(smem + ((kb + 1) & 1) * S::buf_bytes),
                                          goff0 + ((kb + 1) & 1) * kGoffStride, m, beta);
         }
+        OUTER_PROF_T(t1);
         // ---- consume: register accumulation over this warp's runs
         const C* sb = reinterpret_cast<const C*>(smem + (kb & 1) * S::buf_bytes);
         const T* swy = reinterpret_cast<const T*>(sb + B * E);
@@ -252,7 +292,12 @@ __global__ void __launch_bounds__(kOutThreads, OuterMinBlocks<T>::value)
                 }
             }
         }
+        OUTER_PROF_T(t2);
         __syncthreads();  // batch kb consumed, batch kb + 1 produced
+        OUTER_PROF_T(t3);
+        OUTER_PROF_ADD(warp, 0, t1 - t0);
+        OUTER_PROF_ADD(warp, 1, t2 - t1);
+        OUTER_PROF_ADD(warp, 2, t3 - t2);
     }
     // ---- flush: registers -> smem subgrid -> periodic fine grid (bulk reductions)
     const TileX tx = tile_x<sizeof(C)>(bx, TT, W);
@@ -283,6 +328,10 @@ __global__ void __launch_bounds__(kOutThreads, OuterMinBlocks<T>::value)
     }
     bulk_commit();
     bulk_wait_read();  // the staged rows must outlive the bulk reads
+#ifdef NUFFT_OUTER_PROF
+    OUTER_PROF_T(tk1);
+    OUTER_PROF_ADD(threadIdx.x >> 5, 7, tk1 - tk0);
+#endif
 }
 
 template <typename T, int W>
@@ -346,3 +395,15 @@ template size_t spread_outer_smem_bytes<float>(const Geom&);
 template size_t spread_outer_smem_bytes<double>(const Geom&);
 
 }  // namespace nufft
+
+#ifdef NUFFT_OUTER_PROF
+// debug builds only: read (and reset) the per-warp produce / consume / barrier cycles
+extern "C" int nufft_debug_outer_prof(unsigned long long out[64]) {
+    if (cudaMemcpyFromSymbol(out, nufft::g_outer_prof, sizeof(unsigned long long) * 64) !=
+        cudaSuccess)
+        return NUFFT_ERR_CUDA;
+    unsigned long long z[64] = {};
+    return cudaMemcpyToSymbol(nufft::g_outer_prof, z, sizeof(z)) == cudaSuccess ? NUFFT_OK
+                                                                                 : NUFFT_ERR_CUDA;
+}
+#endif

@@ -105,7 +105,8 @@ __global__ void __launch_bounds__(kRowsThreads, 2)
         for (int e = threadIdx.x; e < 3 * W * n; e += kRowsThreads) {
             const int i = e / (3 * W), r3 = e - i * (3 * W), d = r3 / W, k = r3 - d * W;
             const PtRec<T>& r = p.rec[p0 + i];
-            const T wk = es_weight<T>(((T)k - r.d[d]) * two_over_w, beta);
+            const T wk = p.w ? p.w[(size_t)p0 * (3 * W) + e]  // precomputed at setpts
+                             : es_weight<T>(((T)k - r.d[d]) * two_over_w, beta);
             if (d < 2) {
                 swxy[i * 2 * W + d * W + k] = wk;
             } else {

@@ -33,7 +33,8 @@ class Opts(ctypes.Structure):
     _fields_ = [("L", ctypes.c_double), ("modeord", ctypes.c_int), ("stream", ctypes.c_void_p),
                 ("comm", ctypes.c_void_p), ("points_owned", ctypes.c_int),
                 ("tile", ctypes.c_int * 3), ("timing", ctypes.c_int),
-                ("spread_warps", ctypes.c_int), ("reserved", ctypes.c_int * 6)]
+                ("spread_warps", ctypes.c_int), ("precompute", ctypes.c_int),
+                ("reserved", ctypes.c_int * 5)]
 
 
 class Info(ctypes.Structure):
@@ -45,7 +46,8 @@ class Info(ctypes.Structure):
                 ("ms_setpts", ctypes.c_float), ("ms_spread", ctypes.c_float),
                 ("ms_fold", ctypes.c_float), ("ms_fft", ctypes.c_float),
                 ("ms_deconv", ctypes.c_float), ("ms_pad", ctypes.c_float),
-                ("ms_interp", ctypes.c_float), ("ms_comm", ctypes.c_float)]
+                ("ms_interp", ctypes.c_float), ("ms_comm", ctypes.c_float),
+                ("weights_precomputed", ctypes.c_int)]
 
     def as_dict(self):
         d = {}
@@ -150,11 +152,12 @@ class Plan:
     L        : period of the point domain [0, L)^3
     comm     : a Comm -> z-slab plan over its ranks (modes are y-slabs: local_modes())
     points_owned : distributed only; 1 = every point given lies in this rank's z-slab
+    precompute : ES weights per point stored by setpts (0 auto, 1 always, -1 never)
     """
 
     def __init__(self, N, eps, precision="f64", iflag=-1, L=2 * math.pi, modeord=0,
                  device=None, stream=None, tile=None, timing=False, spread_warps=0,
-                 comm=None, points_owned=False):
+                 comm=None, points_owned=False, precompute=0):
         if not torch.cuda.is_available():
             raise NufftError("libnufft requires a CUDA device (no CPU fallback)")
         self.N = tuple(int(n) for n in N)
@@ -172,6 +175,7 @@ class Plan:
         o.stream = self._stream.cuda_stream
         o.timing = 1 if timing else 0
         o.spread_warps = int(spread_warps)
+        o.precompute = int(precompute)
         if comm is not None:
             o.comm = comm._h
             o.points_owned = 1 if points_owned else 0

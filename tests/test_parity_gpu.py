@@ -160,6 +160,25 @@ def test_every_spread_kernel(nb, prec, kernel, eps):
     assert oracle.rel_l2(g2, oracle.type2(x, y, z, np64(fk), eps)) <= TOL[prec]
 
 
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("kernel", [1, 2, 8])
+@pytest.mark.parametrize("precompute", [-1, 1])
+def test_precomputed_weights_both_paths(nb, prec, kernel, precompute):
+    # opts.precompute: ES weights stored by setpts (1) or evaluated in the kernels (-1)
+    eps = 1e-6
+    w = nb.Plan((8, 8, 8), eps, precision=prec).info()["w"]
+    tile = 16 - w if kernel in (1, 2) else 8
+    N, Np = (24, 20, 28), 30000
+    pts, c = host_inputs(Np, prec, seed=12)
+    fk = synthetic.modes(*N).to(c.dtype)
+    plan, g1, g2 = run_pair(nb, N, eps, prec, pts, c, fk, tile=tile, spread_warps=kernel,
+                            precompute=precompute)
+    assert plan.info()["weights_precomputed"] == (1 if precompute == 1 else 0)
+    x, y, z = (np64(p) for p in pts)
+    assert oracle.rel_l2(g1, oracle.type1(x, y, z, np64(c), N, eps)) <= TOL[prec]
+    assert oracle.rel_l2(g2, oracle.type2(x, y, z, np64(fk), eps)) <= TOL[prec]
+
+
 def test_custom_and_ragged_tiles(nb):
     N, Np, eps = (32, 32, 32), 30000, 1e-5
     pts, c = host_inputs(Np, "f64", seed=7)
