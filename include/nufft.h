@@ -127,6 +127,18 @@ int nufft_execute_type1(nufft_handle h, const void* c, void* fk);
  * Pre-correct (D) + zero-pad (chi^T), fused -> FFT with sign -iflag -> interpolate (C^T). */
 int nufft_execute_type2(nufft_handle h, const void* fk, void* c);
 
+/* Real-valued transforms ("all implementations support real and complex-valued inputs",
+ * PAPER.md:198).  Same plan, same points; the spread / interp grid is REAL and the FFT
+ * runs on its half spectrum (R2C / C2R), halving grid bytes, FFT work and FMAs.
+ *   type1_real: c = Np REAL strengths; fk = N1 N2 N3 complex out (Hermitian: fk[-n] =
+ *               conj fk[n]), identical in value to nufft_execute_type1 with c + 0i.
+ *   type2_real: fk = N1 N2 N3 complex in; c = Np REAL out, c_j = Re(sum_n fk[n]
+ *               exp(-iflag i (2 pi / L) n . x_j)) -- the real part of nufft_execute_type2
+ *               (exact when fk is Hermitian, e.g. a Fourier-space field of a real field).
+ * Single-GPU plans only (NUFFT_ERR_UNSUPPORTED on a slab plan for now). */
+int nufft_execute_type1_real(nufft_handle h, const void* c, void* fk);
+int nufft_execute_type2_real(nufft_handle h, const void* fk, void* c);
+
 /* The spreading operator alone (Step 1): grid = C c on the periodic
  * nf1 x nf2 x nf3 fine grid (overwritten).  Single-GPU plans only. */
 int nufft_spread(nufft_handle h, const void* c, void* grid);

@@ -143,20 +143,23 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 }
 
 // Tile x-geometry shared by spread and interp.  Bulk copies need 16-byte
-// aligned rows: fp64 complex cells are 16 bytes, so any origin works (row
-// length = pitch = T + w); fp32 complex cells are 8 bytes, so the subgrid row
-// starts at an EVEN global x and has an even length round_up_even(T + w + 1),
-// and the smem pitch is = 8 (mod 16) cells: two consecutive rows of 8 cells then
-// fill one 128-byte wavefront of 64-bit loads without bank conflicts.
+// aligned rows and lengths.  fp64 complex cells are 16 bytes, so any origin
+// works (row length = pitch = T + w).  Smaller cells (fp32 complex / fp64 real:
+// 8 bytes, fp32 real: 4 bytes) start the subgrid row at a global x that is a
+// multiple of A = 16 / cell_bytes (shift = ox mod A) with a length that is a
+// multiple of A and covers every shift; the smem pitch is = 8 (mod 16) cells, so
+// the 2 (8-byte) or 4 (4-byte) consecutive 8-cell row segments of one 128-byte
+// wavefront fall into distinct banks.
 struct TileX {
     int gx0;    // global x of smem column 0 (may be negative: periodic)
-    int shift;  // smem column of the nominal tile origin bx*T - w/2 (0 or 1)
+    int shift;  // smem column of the nominal tile origin bx*T - w/2 (< 16 / cell bytes)
     int len;    // cells per row copied to / from the grid
     int pitch;  // smem row stride in cells (>= len)
 };
 template <int CELL_BYTES>
 __host__ __device__ __forceinline__ int tile_len(int T, int W) {
-    return CELL_BYTES >= 16 ? T + W : ((T + W + 2) & ~1);
+    constexpr int A = CELL_BYTES >= 16 ? 1 : 16 / CELL_BYTES;
+    return A == 1 ? T + W : ((T + W + (A - 1) + (A - 1)) / A) * A;
 }
 template <int CELL_BYTES>
 __host__ __device__ __forceinline__ int tile_pitch(int T, int W) {
@@ -166,14 +169,33 @@ __host__ __device__ __forceinline__ int tile_pitch(int T, int W) {
 }
 template <int CELL_BYTES>
 __device__ __forceinline__ TileX tile_x(int bx, int T, int W) {
+    constexpr int A = CELL_BYTES >= 16 ? 1 : 16 / CELL_BYTES;
     const int ox = bx * T - W / 2;
     TileX t;
-    t.shift = CELL_BYTES >= 16 ? 0 : (ox & 1);
+    t.shift = ox & (A - 1);
     t.gx0 = ox - t.shift;
     t.len = tile_len<CELL_BYTES>(T, W);
     t.pitch = tile_pitch<CELL_BYTES>(T, W);
     return t;
 }
+
+// ---- grid / strength value types: complex (Eq. 1-2) or real
+__device__ __forceinline__ float2 vscale(float2 a, float s) { return float2{a.x * s, a.y * s}; }
+__device__ __forceinline__ double2 vscale(double2 a, double s) { return double2{a.x * s, a.y * s}; }
+__device__ __forceinline__ float vscale(float a, float s) { return a * s; }
+__device__ __forceinline__ double vscale(double a, double s) { return a * s; }
+// acc += z * w
+__device__ __forceinline__ void vfma(float2& acc, float2 z, float w) {
+    acc.x = fmaf(z.x, w, acc.x);
+    acc.y = fmaf(z.y, w, acc.y);
+}
+__device__ __forceinline__ void vfma(double2& acc, double2 z, double w) {
+    acc.x = fma(z.x, w, acc.x);
+    acc.y = fma(z.y, w, acc.y);
+}
+__device__ __forceinline__ void vfma(float& acc, float z, float w) { acc = fmaf(z, w, acc); }
+__device__ __forceinline__ void vfma(double& acc, double z, double w) { acc = fma(z, w, acc); }
+template <typename V> __device__ __forceinline__ V vzero() { return V{}; }
 
 // Split a periodic row [gx0, gx0 + len) of a row of length nf into at most two
 // contiguous segments; returns the count.  seg_g = global start, seg_s = smem

@@ -92,6 +92,12 @@ template <typename T>
 cudaError_t launch_interp(const Geom& g, const PtsView<T>& p, int64_t nbins,
                           const typename Cx<T>::type* grid, typename Cx<T>::type* c, double beta,
                           cudaStream_t s);
+template <typename T>
+cudaError_t launch_spread_real(const Geom& g, const PtsView<T>& p, int64_t nbins, const T* c,
+                               T* grid, double beta, cudaStream_t s);
+template <typename T>
+cudaError_t launch_interp_real(const Geom& g, const PtsView<T>& p, int64_t nbins, const T* grid,
+                               T* c, double beta, cudaStream_t s);
 template <typename T> size_t spread_smem_bytes(const Geom& g);
 // spread_rows.cu: register-row spread (default when w <= 12 and T = 16 - w on every axis)
 bool spread_rows_applies(const Geom& g);
@@ -106,6 +112,9 @@ template <typename T>
 cudaError_t launch_spread_outer(const Geom& g, const PtsView<T>& p, int64_t nbins,
                                 const typename Cx<T>::type* c, typename Cx<T>::type* grid,
                                 double beta, cudaStream_t s);
+template <typename T>
+cudaError_t launch_spread_outer_real(const Geom& g, const PtsView<T>& p, int64_t nbins,
+                                     const T* c, T* grid, double beta, cudaStream_t s);
 template <typename T> size_t spread_outer_smem_bytes(const Geom& g);
 template <typename T> size_t interp_smem_bytes(const Geom& g);
 // elementwise.cu
@@ -118,6 +127,18 @@ cudaError_t launch_pad_precorrect(const typename Cx<T>::type* fk, const int64_t 
                                   const T* p1, const T* p2, const T* p3, int modeord,
                                   const int64_t nf[3], typename Cx<T>::type* grid,
                                   cudaStream_t s);
+
+// real-valued transforms: R2C half spectrum H (nf3 x nf2 x (nf1/2 + 1), x fastest)
+template <typename T>
+cudaError_t launch_truncate_deconv_r2c(const typename Cx<T>::type* H, const int64_t nf[3],
+                                       const int64_t N[3], const T* p1, const T* p2, const T* p3,
+                                       int modeord, int conj_all, typename Cx<T>::type* fk,
+                                       cudaStream_t s);
+template <typename T>
+cudaError_t launch_pad_precorrect_c2r(const typename Cx<T>::type* fk, const int64_t N[3],
+                                      const T* p1, const T* p2, const T* p3, int modeord,
+                                      int sign_plus, const int64_t nf[3],
+                                      typename Cx<T>::type* H, cudaStream_t s);
 
 // host-side window helpers (plan.cu)
 int select_width(double eps, int precision, int* w, double* beta, double* eps_used);

@@ -34,9 +34,10 @@ using namespace dev;
 constexpr int kInterpThreads = 256;
 constexpr int kInterpWarps = kInterpThreads / 32;
 
-template <typename T, int W>
+// V: value type of the grid and of the outputs, Cx<T> (complex) or T (real)
+template <typename T, typename V, int W>
 struct InterpSmem {
-    using C = typename Cx<T>::type;
+    using C = V;
     // per-point weight stride in elements, ODD: lane l stores its point's weights
     // at l * WS, so the 32 (fp32) / 16 (fp64 half-warp) lanes of a store hit
     // distinct banks (an even stride such as 16 at w = 5 serialises them 16-32 way)
@@ -46,15 +47,30 @@ struct InterpSmem {
     }
 };
 
-template <typename T, int W>
+__device__ __forceinline__ float vre(float2 v) { return v.x; }
+__device__ __forceinline__ double vre(double2 v) { return v.x; }
+__device__ __forceinline__ float vre(float v) { return v; }
+__device__ __forceinline__ double vre(double v) { return v; }
+__device__ __forceinline__ float vim(float2 v) { return v.y; }
+__device__ __forceinline__ double vim(double2 v) { return v.y; }
+__device__ __forceinline__ float vim(float) { return 0.f; }
+__device__ __forceinline__ double vim(double) { return 0.0; }
+template <typename V, typename T> __device__ __forceinline__ V vmake(T re, T im);
+template <> __device__ __forceinline__ float2 vmake<float2, float>(float re, float im) { return float2{re, im}; }
+template <> __device__ __forceinline__ double2 vmake<double2, double>(double re, double im) { return double2{re, im}; }
+template <> __device__ __forceinline__ float vmake<float, float>(float re, float) { return re; }
+template <> __device__ __forceinline__ double vmake<double, double>(double re, double) { return re; }
+
+template <typename T, typename V, int W>
 __global__ void __launch_bounds__(kInterpThreads, 2)
-    interp_tile_kernel(Geom g, PtsView<T> p, const typename Cx<T>::type* __restrict__ grid,
-                       typename Cx<T>::type* __restrict__ out, T beta) {
-    using C = typename Cx<T>::type;
+    interp_tile_kernel(Geom g, PtsView<T> p, const V* __restrict__ grid, V* __restrict__ out,
+                       T beta) {
+    using C = V;
+    constexpr bool kReal = sizeof(V) == sizeof(T);
     constexpr bool kFlat = W <= 5;
     constexpr int NQ = kFlat ? (W * W + 31) / 32 : 1;
     constexpr int XS = W <= 8 ? 8 : 16, YS = 32 / XS, NPASS = (W + YS - 1) / YS;
-    constexpr int WS = InterpSmem<T, W>::WS;
+    constexpr int WS = InterpSmem<T, V, W>::WS;
     constexpr int NW = kInterpWarps;
     extern __shared__ __align__(16) unsigned char smem[];
 
@@ -177,12 +193,12 @@ __global__ void __launch_bounds__(kInterpThreads, 2)
 #pragma unroll
                                 for (int k = 0; k < W; ++k) {
                                     const C v = col[k * plane];
-                                    sr += v.x * wz[k];
-                                    si += v.y * wz[k];
+                                    sr += vre(v) * wz[k];
+                                    if constexpr (!kReal) si += vim(v) * wz[k];
                                 }
                                 const T wxy = wj[qx[q]] * wj[W + qy[q]];
                                 vr[g4] += sr * wxy;
-                                vi[g4] += si * wxy;
+                                if constexpr (!kReal) vi[g4] += si * wxy;
                             }
                         }
                     } else {
@@ -196,38 +212,40 @@ __global__ void __launch_bounds__(kInterpThreads, 2)
 #pragma unroll
                                 for (int k = 0; k < W; ++k) {
                                     const C v = col[k * plane];
-                                    sr += v.x * wz[k];
-                                    si += v.y * wz[k];
+                                    sr += vre(v) * wz[k];
+                                    if constexpr (!kReal) si += vim(v) * wz[k];
                                 }
                                 const T wy = wj[W + y];
                                 vr[g4] += sr * wy;
-                                vi[g4] += si * wy;
+                                if constexpr (!kReal) vi[g4] += si * wy;
                             }
                         }
                         const T wx = sx < W ? wj[sx] : (T)0;
                         vr[g4] *= wx;
-                        vi[g4] *= wx;
+                        if constexpr (!kReal) vi[g4] *= wx;
                     }
                 }
             }
             const bool h16 = lane & 16, h8 = lane & 8;
             T r0 = h16 ? vr[1] : vr[0], r1 = h16 ? vr[3] : vr[2];
-            T i0 = h16 ? vi[1] : vi[0], i1 = h16 ? vi[3] : vi[2];
             r0 += __shfl_xor_sync(0xffffffffu, h16 ? vr[0] : vr[1], 16);
             r1 += __shfl_xor_sync(0xffffffffu, h16 ? vr[2] : vr[3], 16);
-            i0 += __shfl_xor_sync(0xffffffffu, h16 ? vi[0] : vi[1], 16);
-            i1 += __shfl_xor_sync(0xffffffffu, h16 ? vi[2] : vi[3], 16);
-            T rr = h8 ? r1 : r0, ii = h8 ? i1 : i0;
+            T rr = h8 ? r1 : r0, ii = 0;
             rr += __shfl_xor_sync(0xffffffffu, h8 ? r0 : r1, 8);
-            ii += __shfl_xor_sync(0xffffffffu, h8 ? i0 : i1, 8);
 #pragma unroll
-            for (int o = 4; o > 0; o >>= 1) {
-                rr += __shfl_xor_sync(0xffffffffu, rr, o);
-                ii += __shfl_xor_sync(0xffffffffu, ii, o);
+            for (int o = 4; o > 0; o >>= 1) rr += __shfl_xor_sync(0xffffffffu, rr, o);
+            if constexpr (!kReal) {
+                T i0 = h16 ? vi[1] : vi[0], i1 = h16 ? vi[3] : vi[2];
+                i0 += __shfl_xor_sync(0xffffffffu, h16 ? vi[0] : vi[1], 16);
+                i1 += __shfl_xor_sync(0xffffffffu, h16 ? vi[2] : vi[3], 16);
+                ii = h8 ? i1 : i0;
+                ii += __shfl_xor_sync(0xffffffffu, h8 ? i0 : i1, 8);
+#pragma unroll
+                for (int o = 4; o > 0; o >>= 1) ii += __shfl_xor_sync(0xffffffffu, ii, o);
             }
             const int j = j0 + (h16 ? 1 : 0) + (h8 ? 2 : 0);
             const uint32_t pj = __shfl_sync(0xffffffffu, my_perm, j & 31);
-            if ((lane & 7) == 0 && j < np) out[pj] = C{rr, ii};
+            if ((lane & 7) == 0 && j < np) out[pj] = vmake<C, T>(rr, ii);
         }
         __syncwarp();
     }
@@ -236,19 +254,17 @@ __global__ void __launch_bounds__(kInterpThreads, 2)
     if (!staged) mbar_wait(bar, 0);
 }
 
-template <typename T, int W>
+template <typename T, typename V, int W>
 size_t smem_w(const Geom& g) {
-    using C = typename Cx<T>::type;
-    return InterpSmem<T, W>::bytes(tile_pitch<sizeof(C)>(g.T[0], W) * (g.T[1] + W) *
-                                   (g.T[2] + W));
+    return InterpSmem<T, V, W>::bytes(tile_pitch<sizeof(V)>(g.T[0], W) * (g.T[1] + W) *
+                                      (g.T[2] + W));
 }
 
-template <typename T, int W>
-cudaError_t launch_w(const Geom& g, const PtsView<T>& p, int64_t nbins,
-                     const typename Cx<T>::type* grid, typename Cx<T>::type* c, double beta,
-                     cudaStream_t s) {
-    const size_t smem = smem_w<T, W>(g);
-    auto kern = interp_tile_kernel<T, W>;
+template <typename T, typename V, int W>
+cudaError_t launch_w(const Geom& g, const PtsView<T>& p, int64_t nbins, const V* grid, V* c,
+                     double beta, cudaStream_t s) {
+    const size_t smem = smem_w<T, V, W>(g);
+    auto kern = interp_tile_kernel<T, V, W>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) {
@@ -275,7 +291,16 @@ template <typename T>
 cudaError_t launch_interp(const Geom& g, const PtsView<T>& p, int64_t nbins,
                           const typename Cx<T>::type* grid, typename Cx<T>::type* c, double beta,
                           cudaStream_t s) {
-#define CALL(WW) launch_w<T, WW>(g, p, nbins, grid, c, beta, s)
+#define CALL(WW) launch_w<T, typename Cx<T>::type, WW>(g, p, nbins, grid, c, beta, s)
+    NUFFT_W_SWITCH(CALL)
+#undef CALL
+    return cudaErrorInvalidValue;
+}
+
+template <typename T>
+cudaError_t launch_interp_real(const Geom& g, const PtsView<T>& p, int64_t nbins, const T* grid,
+                               T* c, double beta, cudaStream_t s) {
+#define CALL(WW) launch_w<T, T, WW>(g, p, nbins, grid, c, beta, s)
     NUFFT_W_SWITCH(CALL)
 #undef CALL
     return cudaErrorInvalidValue;
@@ -283,7 +308,7 @@ cudaError_t launch_interp(const Geom& g, const PtsView<T>& p, int64_t nbins,
 
 template <typename T>
 size_t interp_smem_bytes(const Geom& g) {
-#define CALL(WW) smem_w<T, WW>(g)
+#define CALL(WW) smem_w<T, typename Cx<T>::type, WW>(g)
     NUFFT_W_SWITCH(CALL)
 #undef CALL
     return 0;
@@ -293,6 +318,10 @@ template cudaError_t launch_interp<float>(const Geom&, const PtsView<float>&, in
                                           const float2*, float2*, double, cudaStream_t);
 template cudaError_t launch_interp<double>(const Geom&, const PtsView<double>&, int64_t,
                                            const double2*, double2*, double, cudaStream_t);
+template cudaError_t launch_interp_real<float>(const Geom&, const PtsView<float>&, int64_t,
+                                               const float*, float*, double, cudaStream_t);
+template cudaError_t launch_interp_real<double>(const Geom&, const PtsView<double>&, int64_t,
+                                                const double*, double*, double, cudaStream_t);
 template size_t interp_smem_bytes<float>(const Geom&);
 template size_t interp_smem_bytes<double>(const Geom&);
 

@@ -266,6 +266,68 @@ int do_spread(nufft_plan_s* p, const void* c_dev, void* grid0) {
     return NUFFT_OK;
 }
 
+// real-valued transforms: real strengths / grid / outputs
+int do_spread_real(nufft_plan_s* p, const void* c_dev, void* grid) {
+    StageTimer tm(p, EV_SPREAD);
+    Geom g = p->geom;
+    if (g.spread_warps == 1) g.spread_warps = 8;  // no real register-row kernel
+    if (g.spread_warps == 2 && p->prec == NUFFT_F64)
+        NUFFT_CK(launch_spread_outer_real<double>(g, pts_view<double>(p), p->nbins,
+                                                  static_cast<const double*>(c_dev),
+                                                  static_cast<double*>(grid), p->beta, p->stream));
+    else if (g.spread_warps == 2)
+        NUFFT_CK(launch_spread_outer_real<float>(g, pts_view<float>(p), p->nbins,
+                                                 static_cast<const float*>(c_dev),
+                                                 static_cast<float*>(grid), p->beta, p->stream));
+    else if (p->prec == NUFFT_F64)
+        NUFFT_CK(launch_spread_real<double>(g, pts_view<double>(p), p->nbins,
+                                            static_cast<const double*>(c_dev),
+                                            static_cast<double*>(grid), p->beta, p->stream));
+    else
+        NUFFT_CK(launch_spread_real<float>(g, pts_view<float>(p), p->nbins,
+                                           static_cast<const float*>(c_dev),
+                                           static_cast<float*>(grid), p->beta, p->stream));
+    return NUFFT_OK;
+}
+
+int do_interp_real(nufft_plan_s* p, const void* grid, void* c_dev) {
+    StageTimer tm(p, EV_INTERP);
+    if (p->prec == NUFFT_F64)
+        NUFFT_CK(launch_interp_real<double>(p->geom, pts_view<double>(p), p->nbins,
+                                            static_cast<const double*>(grid),
+                                            static_cast<double*>(c_dev), p->beta, p->stream));
+    else
+        NUFFT_CK(launch_interp_real<float>(p->geom, pts_view<float>(p), p->nbins,
+                                           static_cast<const float*>(grid),
+                                           static_cast<float*>(c_dev), p->beta, p->stream));
+    return NUFFT_OK;
+}
+
+int ensure_real_fft(nufft_plan_s* p) {
+    if (p->fft_r_ok) return NUFFT_OK;
+    const bool f64 = p->prec == NUFFT_F64;
+    const int n3 = (int)p->nf[2], n2 = (int)p->nf[1], n1 = (int)p->nf[0];
+    if (cufftPlan3d(&p->fft_r2c, n3, n2, n1, f64 ? CUFFT_D2Z : CUFFT_R2C) != CUFFT_SUCCESS)
+        return NUFFT_ERR_CUFFT;
+    if (cufftPlan3d(&p->fft_c2r, n3, n2, n1, f64 ? CUFFT_Z2D : CUFFT_C2R) != CUFFT_SUCCESS) {
+        cufftDestroy(p->fft_r2c);
+        return NUFFT_ERR_CUFFT;
+    }
+    p->fft_r_ok = true;
+    size_t w1 = 0, w2 = 0;
+    cufftGetSize(p->fft_r2c, &w1);
+    cufftGetSize(p->fft_c2r, &w2);
+    p->bytes += w1 + w2;
+    if (cufftSetStream(p->fft_r2c, p->stream) != CUFFT_SUCCESS ||
+        cufftSetStream(p->fft_c2r, p->stream) != CUFFT_SUCCESS)
+        return NUFFT_ERR_CUFFT;
+    return NUFFT_OK;
+}
+
+void* half_spectrum(nufft_plan_s* p) {
+    return static_cast<char*>(p->d_grid) + (size_t)(p->nf[0] * p->nf[1] * p->nf[2]) * p->real_size;
+}
+
 int do_interp(nufft_plan_s* p, const void* grid0, void* c_dev) {
     StageTimer tm(p, EV_INTERP);
     if (p->prec == NUFFT_F64)
@@ -458,7 +520,10 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
         st = dist_init(p);  // z-slab geometry, halo grid, buffers, slab FFT plans
     } else if (!st) {
         p->nbins = (int64_t)g.nb[0] * g.nb[1] * g.nb[2];
-        p->grid_bytes = (size_t)(p->nf[0] * p->nf[1] * p->nf[2]) * p->cplx_size;
+        // complex grid, or (real transforms) real grid + R2C half spectrum: nf^3 r +
+        // nf3 nf2 (nf1/2 + 1) 2r bytes = complex size + 2 nf2 nf3 r
+        p->grid_bytes = (size_t)(p->nf[0] * p->nf[1] * p->nf[2]) * p->cplx_size +
+                        (size_t)(2 * p->nf[1] * p->nf[2]) * p->real_size;
         st = dev_alloc(p, &p->d_grid, p->grid_bytes);
         p->grid0 = p->d_grid;
         if (!st) {
@@ -573,6 +638,98 @@ int nufft_execute_type2(nufft_handle p, const void* fk, void* c) {
     return finish_output(p, c, cd, c_bytes, staged);
 }
 
+int nufft_execute_type1_real(nufft_handle p, const void* c, void* fk) {
+    cudaGetLastError();
+    if (!p || !fk) return NUFFT_ERR_ARG;
+    if (p->Np < 0) return NUFFT_ERR_NOT_SET;
+    if (!c && user_np(p) > 0) return NUFFT_ERR_ARG;
+    if (p->dist) return NUFFT_ERR_UNSUPPORTED;
+    int st;
+    if ((st = ensure_real_fft(p))) return st;
+    const void* cd = nullptr;
+    if ((st = input_view(p, c, (size_t)p->Np * p->real_size, 0, (size_t)p->Np * p->real_size, &cd)))
+        return st;
+    const size_t fk_bytes = (size_t)(p->N[0] * p->N[1] * p->N[2]) * p->cplx_size;
+    void* fkd = nullptr;
+    bool staged = false;
+    if ((st = output_view(p, fk, fk_bytes, &fkd, &staged))) return st;
+    const size_t rg = (size_t)(p->nf[0] * p->nf[1] * p->nf[2]) * p->real_size;
+    NUFFT_CK(cudaMemsetAsync(p->d_grid, 0, rg, p->stream));
+    if ((st = do_spread_real(p, cd, p->d_grid))) return st;              // Step 1: C
+    {
+        StageTimer tm(p, EV_FFT);                                        // Step 2: F (R2C)
+        const cufftResult r =
+            p->prec == NUFFT_F64
+                ? cufftExecD2Z(p->fft_r2c, static_cast<cufftDoubleReal*>(p->d_grid),
+                               static_cast<cufftDoubleComplex*>(half_spectrum(p)))
+                : cufftExecR2C(p->fft_r2c, static_cast<cufftReal*>(p->d_grid),
+                               static_cast<cufftComplex*>(half_spectrum(p)));
+        if (r != CUFFT_SUCCESS) return NUFFT_ERR_CUFFT;
+    }
+    {
+        StageTimer tm(p, EV_DECONV);                                     // Steps 3, 4
+        const int conj_all = p->iflag > 0 ? 1 : 0;
+        if (p->prec == NUFFT_F64)
+            NUFFT_CK(launch_truncate_deconv_r2c<double>(
+                static_cast<const double2*>(half_spectrum(p)), p->nf, p->N,
+                static_cast<const double*>(p->d_p[0]), static_cast<const double*>(p->d_p[1]),
+                static_cast<const double*>(p->d_p[2]), p->modeord, conj_all,
+                static_cast<double2*>(fkd), p->stream));
+        else
+            NUFFT_CK(launch_truncate_deconv_r2c<float>(
+                static_cast<const float2*>(half_spectrum(p)), p->nf, p->N,
+                static_cast<const float*>(p->d_p[0]), static_cast<const float*>(p->d_p[1]),
+                static_cast<const float*>(p->d_p[2]), p->modeord, conj_all,
+                static_cast<float2*>(fkd), p->stream));
+    }
+    return finish_output(p, fk, fkd, fk_bytes, staged);
+}
+
+int nufft_execute_type2_real(nufft_handle p, const void* fk, void* c) {
+    cudaGetLastError();
+    if (!p || !fk) return NUFFT_ERR_ARG;
+    if (p->Np < 0) return NUFFT_ERR_NOT_SET;
+    if (!c && user_np(p) > 0) return NUFFT_ERR_ARG;
+    if (p->dist) return NUFFT_ERR_UNSUPPORTED;
+    int st;
+    if ((st = ensure_real_fft(p))) return st;
+    const size_t fk_bytes = (size_t)(p->N[0] * p->N[1] * p->N[2]) * p->cplx_size;
+    const void* fkd = nullptr;
+    if ((st = input_view(p, fk, fk_bytes, 0, fk_bytes, &fkd))) return st;
+    const size_t c_bytes = (size_t)p->Np * p->real_size;
+    void* cd = nullptr;
+    bool staged = false;
+    if ((st = output_view(p, c, c_bytes, &cd, &staged))) return st;
+    {
+        StageTimer tm(p, EV_PAD);                                        // D, chi^T, Hermitian part
+        const int sign_plus = p->iflag < 0 ? 1 : 0;                      // type-2 sign = -iflag
+        if (p->prec == NUFFT_F64)
+            NUFFT_CK(launch_pad_precorrect_c2r<double>(
+                static_cast<const double2*>(fkd), p->N, static_cast<const double*>(p->d_p[0]),
+                static_cast<const double*>(p->d_p[1]), static_cast<const double*>(p->d_p[2]),
+                p->modeord, sign_plus, p->nf, static_cast<double2*>(half_spectrum(p)),
+                p->stream));
+        else
+            NUFFT_CK(launch_pad_precorrect_c2r<float>(
+                static_cast<const float2*>(fkd), p->N, static_cast<const float*>(p->d_p[0]),
+                static_cast<const float*>(p->d_p[1]), static_cast<const float*>(p->d_p[2]),
+                p->modeord, sign_plus, p->nf, static_cast<float2*>(half_spectrum(p)),
+                p->stream));
+    }
+    {
+        StageTimer tm(p, EV_FFT);                                        // F^-1 (C2R)
+        const cufftResult r =
+            p->prec == NUFFT_F64
+                ? cufftExecZ2D(p->fft_c2r, static_cast<cufftDoubleComplex*>(half_spectrum(p)),
+                               static_cast<cufftDoubleReal*>(p->d_grid))
+                : cufftExecC2R(p->fft_c2r, static_cast<cufftComplex*>(half_spectrum(p)),
+                               static_cast<cufftReal*>(p->d_grid));
+        if (r != CUFFT_SUCCESS) return NUFFT_ERR_CUFFT;
+    }
+    if ((st = do_interp_real(p, p->d_grid, cd))) return st;              // C^T
+    return finish_output(p, c, cd, c_bytes, staged);
+}
+
 int nufft_spread(nufft_handle p, const void* c, void* grid) {
     cudaGetLastError();  // a stale non-sticky error of another caller is not ours
     if (!p || !grid || (!c && p->Np > 0)) return NUFFT_ERR_ARG;
@@ -612,6 +769,10 @@ int nufft_destroy(nufft_handle p) {
     else cudaDeviceSynchronize();
     if (p->dist) dist_destroy(p);
     if (p->fft_ok) cufftDestroy(p->fft);
+    if (p->fft_r_ok) {
+        cufftDestroy(p->fft_r2c);
+        cufftDestroy(p->fft_c2r);
+    }
     for (int d = 0; d < 3; ++d) dev_free(p, &p->d_p[d], 0);
     dev_free(p, &p->d_grid, 0);
     dev_free(p, (void**)&p->count, 0);

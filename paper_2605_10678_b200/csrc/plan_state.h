@@ -36,6 +36,10 @@ struct nufft_plan_s {
     void* grid0 = nullptr;    // local plane 0 of the grid (== d_grid on one GPU)
     cufftHandle fft = 0;      // one GPU: 3D plan
     bool fft_ok = false;
+    // real-valued transforms (one GPU): R2C / C2R plans, created on first use; the
+    // real grid is d_grid[0, nf^3) reals, the half spectrum follows it
+    cufftHandle fft_r2c = 0, fft_c2r = 0;
+    bool fft_r_ok = false;
 
     // points (this rank's, after redistribution)
     int64_t Np = -1;

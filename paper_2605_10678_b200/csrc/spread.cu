@@ -42,9 +42,10 @@ template <typename T> struct Batch;
 template <> struct Batch<float> { static constexpr int value = 64; };
 template <> struct Batch<double> { static constexpr int value = 32; };
 
-template <typename T, int W>
+// V: value type of strengths and grid cells, Cx<T> (complex) or T (real)
+template <typename T, typename V, int W>
 struct SpreadSmem {
-    using C = typename Cx<T>::type;
+    using C = V;
     static constexpr int B = Batch<T>::value;
     static constexpr int NQ = (W * W + 31) / 32;
     // per point: wxy[NQ*32] reals (by lane slot), cwz[W] complex, strength, 1D weights
@@ -56,12 +57,12 @@ struct SpreadSmem {
     static size_t bytes(int ncell) { return (size_t)ncell * sizeof(C) + batch_bytes(); }
 };
 
-template <typename T, int W, int NW>
+template <typename T, typename V, int W, int NW>
 __global__ void __launch_bounds__(32 * NW)
-    spread_tile_kernel(Geom g, PtsView<T> p, const typename Cx<T>::type* __restrict__ c,
-                       typename Cx<T>::type* __restrict__ grid, T beta) {
-    using C = typename Cx<T>::type;
-    using S = SpreadSmem<T, W>;
+    spread_tile_kernel(Geom g, PtsView<T> p, const V* __restrict__ c, V* __restrict__ grid,
+                       T beta) {
+    using C = V;
+    using S = SpreadSmem<T, V, W>;
     constexpr int B = S::B;
     constexpr int NQ = S::NQ;
     constexpr int kSpreadThreads = 32 * NW;
@@ -83,7 +84,7 @@ __global__ void __launch_bounds__(32 * NW)
     int* sbase = reinterpret_cast<int*>(sw1d + B * 3 * W); // [B]
     int* slz = sbase + B;                                  // [B]
 
-    for (int i = threadIdx.x; i < ncell; i += kSpreadThreads) tile[i] = C{0, 0};
+    for (int i = threadIdx.x; i < ncell; i += kSpreadThreads) tile[i] = vzero<C>();
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int qoff[NQ];
@@ -125,7 +126,7 @@ __global__ void __launch_bounds__(32 * NW)
             const int i = e / W, k = e - i * W;
             const T wz = sw1d[i * 3 * W + 2 * W + k];
             const C cv = scv[i];
-            scwz[e] = C{cv.x * wz, cv.y * wz};
+            scwz[e] = vscale(cv, wz);
         }
         __syncthreads();
         // ---- phase B: warp-owned z-planes {z : z % NW == warp}
@@ -145,8 +146,7 @@ __global__ void __launch_bounds__(32 * NW)
                     if (qok[q]) {
                         C* cell = row + qoff[q];
                         C v = *cell;
-                        v.x += cv.x * wq[q];
-                        v.y += cv.y * wq[q];
+                        vfma(v, cv, wq[q]);
                         *cell = v;
                     }
                 }
@@ -174,19 +174,17 @@ __global__ void __launch_bounds__(32 * NW)
     bulk_wait_read();  // the subgrid must outlive the bulk reads
 }
 
-template <typename T, int W>
+template <typename T, typename V, int W>
 size_t smem_w(const Geom& g) {
-    using C = typename Cx<T>::type;
-    return SpreadSmem<T, W>::bytes(tile_pitch<sizeof(C)>(g.T[0], W) * (g.T[1] + W) *
-                                   (g.T[2] + W));
+    return SpreadSmem<T, V, W>::bytes(tile_pitch<sizeof(V)>(g.T[0], W) * (g.T[1] + W) *
+                                      (g.T[2] + W));
 }
 
-template <typename T, int W, int NW>
-cudaError_t launch_nw(const Geom& g, const PtsView<T>& p, int64_t nbins,
-                     const typename Cx<T>::type* c, typename Cx<T>::type* grid, double beta,
-                     cudaStream_t s) {
-    const size_t smem = smem_w<T, W>(g);
-    auto kern = spread_tile_kernel<T, W, NW>;
+template <typename T, typename V, int W, int NW>
+cudaError_t launch_nw(const Geom& g, const PtsView<T>& p, int64_t nbins, const V* c, V* grid,
+                      double beta, cudaStream_t s) {
+    const size_t smem = smem_w<T, V, W>(g);
+    auto kern = spread_tile_kernel<T, V, W, NW>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) {
@@ -197,12 +195,11 @@ cudaError_t launch_nw(const Geom& g, const PtsView<T>& p, int64_t nbins,
     return cudaGetLastError();
 }
 
-template <typename T, int W>
-cudaError_t launch_w(const Geom& g, const PtsView<T>& p, int64_t nbins,
-                     const typename Cx<T>::type* c, typename Cx<T>::type* grid, double beta,
-                     cudaStream_t s) {
-    return g.spread_warps == 8 ? launch_nw<T, W, 8>(g, p, nbins, c, grid, beta, s)
-                               : launch_nw<T, W, 4>(g, p, nbins, c, grid, beta, s);
+template <typename T, typename V, int W>
+cudaError_t launch_w(const Geom& g, const PtsView<T>& p, int64_t nbins, const V* c, V* grid,
+                     double beta, cudaStream_t s) {
+    return g.spread_warps == 8 ? launch_nw<T, V, W, 8>(g, p, nbins, c, grid, beta, s)
+                               : launch_nw<T, V, W, 4>(g, p, nbins, c, grid, beta, s);
 }
 
 }  // namespace
@@ -221,7 +218,16 @@ template <typename T>
 cudaError_t launch_spread(const Geom& g, const PtsView<T>& p, int64_t nbins,
                           const typename Cx<T>::type* c, typename Cx<T>::type* grid, double beta,
                           cudaStream_t s) {
-#define CALL(WW) launch_w<T, WW>(g, p, nbins, c, grid, beta, s)
+#define CALL(WW) launch_w<T, typename Cx<T>::type, WW>(g, p, nbins, c, grid, beta, s)
+    NUFFT_W_SWITCH(CALL)
+#undef CALL
+    return cudaErrorInvalidValue;
+}
+
+template <typename T>
+cudaError_t launch_spread_real(const Geom& g, const PtsView<T>& p, int64_t nbins, const T* c,
+                               T* grid, double beta, cudaStream_t s) {
+#define CALL(WW) launch_w<T, T, WW>(g, p, nbins, c, grid, beta, s)
     NUFFT_W_SWITCH(CALL)
 #undef CALL
     return cudaErrorInvalidValue;
@@ -229,7 +235,7 @@ cudaError_t launch_spread(const Geom& g, const PtsView<T>& p, int64_t nbins,
 
 template <typename T>
 size_t spread_smem_bytes(const Geom& g) {
-#define CALL(WW) smem_w<T, WW>(g)
+#define CALL(WW) smem_w<T, typename Cx<T>::type, WW>(g)
     NUFFT_W_SWITCH(CALL)
 #undef CALL
     return 0;
@@ -239,6 +245,10 @@ template cudaError_t launch_spread<float>(const Geom&, const PtsView<float>&, in
                                           const float2*, float2*, double, cudaStream_t);
 template cudaError_t launch_spread<double>(const Geom&, const PtsView<double>&, int64_t,
                                            const double2*, double2*, double, cudaStream_t);
+template cudaError_t launch_spread_real<float>(const Geom&, const PtsView<float>&, int64_t,
+                                               const float*, float*, double, cudaStream_t);
+template cudaError_t launch_spread_real<double>(const Geom&, const PtsView<double>&, int64_t,
+                                                const double*, double*, double, cudaStream_t);
 template size_t spread_smem_bytes<float>(const Geom&);
 template size_t spread_smem_bytes<double>(const Geom&);
 

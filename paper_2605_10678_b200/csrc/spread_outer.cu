@@ -52,12 +52,16 @@ template <typename T> struct OuterBatch;
 template <> struct OuterBatch<float> { static constexpr int value = 128; };
 template <> struct OuterBatch<double> { static constexpr int value = 64; };
 
-template <typename T, int W>
+// V: value type of strengths and grid cells, Cx<T> (complex) or T (real)
+template <typename T, typename V, int W>
 struct OuterSmem {
-    using C = typename Cx<T>::type;
+    using C = V;
     static constexpr int E = kOutE;
     static constexpr int B = OuterBatch<T>::value;
-    static constexpr int P = sizeof(C) >= 16 ? E : E + 2;  // staging x pitch (fp32: even-x shift)
+    // staging x pitch: cells of < 16 bytes start the row at a 16-byte aligned global x
+    // (shift < A = 16 / cell bytes columns), so the row gets A extra cells
+    static constexpr int A = sizeof(C) >= 16 ? 1 : 16 / (int)sizeof(C);
+    static constexpr int P = A == 1 ? E : E + A;
     static constexpr size_t tile_bytes = (size_t)E * E * P * sizeof(C);
     // one buffer: b = c wx [B][E] complex | wy [B][E] | wz [B][E]
     static constexpr size_t buf_bytes = (size_t)B * E * (sizeof(C) + 2 * sizeof(T));
@@ -102,9 +106,9 @@ __device__ __forceinline__ void group_sync() {
     else asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NT) : "memory");
 }
 
-template <typename T>
+template <typename T, typename V>
 struct OuterPtrs {
-    using C = typename Cx<T>::type;
+    using C = V;
     C* sc;       // [B]    strength
     T* sd;       // [B][4] phase offsets
     int* sla;    // [B]    packed stencil base
@@ -116,13 +120,12 @@ struct OuterPtrs {
 // Produce one batch into buffer `buf` (b | wy | wz) and its key starts `goff`,
 // using NT threads (tid in [0, NT)) synchronised by barrier BAR.  No trailing
 // barrier: the caller's CTA barrier publishes the batch.
-template <typename T, int W, int NT, int BAR>
-__device__ __forceinline__ void produce(int tid, const PtsView<T>& p,
-                                        const typename Cx<T>::type* __restrict__ c,
+template <typename T, typename V, int W, int NT, int BAR>
+__device__ __forceinline__ void produce(int tid, const PtsView<T>& p, const V* __restrict__ c,
                                         uint32_t p0, int n, T* buf, int* goff,
-                                        const OuterPtrs<T>& m, T beta) {
-    using C = typename Cx<T>::type;
-    using S = OuterSmem<T, W>;
+                                        const OuterPtrs<T, V>& m, T beta) {
+    using C = V;
+    using S = OuterSmem<T, V, W>;
     constexpr int E = kOutE, B = S::B, TT = E - W, NK = 3 * (TT + 1);
     C* sb = reinterpret_cast<C*>(buf);
     T* swy = reinterpret_cast<T*>(sb + B * E);
@@ -184,7 +187,7 @@ __device__ __forceinline__ void produce(int tid, const PtsView<T>& p,
             const C cv = m.sc[t];
             C* row = sb + pos * E + x0;
 #pragma unroll
-            for (int k = 0; k < W; ++k) row[k] = C{cv.x * wk[k], cv.y * wk[k]};
+            for (int k = 0; k < W; ++k) row[k] = vscale(cv, wk[k]);
         } else {
             T* row = swy + (d - 1) * B * E + pos * E + x0;  // d = 1: wy, d = 2: wz
 #pragma unroll
@@ -208,12 +211,12 @@ __device__ __forceinline__ void produce(int tid, const PtsView<T>& p,
 // at low density (one batch per bin)
 template <typename T> struct OuterMinBlocks { static constexpr int value = sizeof(T) == 4 ? 3 : 2; };
 
-template <typename T, int W>
+template <typename T, typename V, int W>
 __global__ void __launch_bounds__(kOutThreads, OuterMinBlocks<T>::value)
-    spread_outer_kernel(Geom g, PtsView<T> p, const typename Cx<T>::type* __restrict__ c,
-                        typename Cx<T>::type* __restrict__ grid, T beta) {
-    using C = typename Cx<T>::type;
-    using S = OuterSmem<T, W>;
+    spread_outer_kernel(Geom g, PtsView<T> p, const V* __restrict__ c, V* __restrict__ grid,
+                        T beta) {
+    using C = V;
+    using S = OuterSmem<T, V, W>;
     constexpr int E = kOutE;
     constexpr int P = S::P;
     constexpr int B = S::B;
@@ -228,7 +231,7 @@ __global__ void __launch_bounds__(kOutThreads, OuterMinBlocks<T>::value)
 
     const int bx = b % g.nb[0], by = (b / g.nb[0]) % g.nb[1], bz = b / (g.nb[0] * g.nb[1]);
     // double-buffered staging: buffer i at smem + i * buf_bytes, key starts goff0 + i * stride
-    OuterPtrs<T> m;
+    OuterPtrs<T, V> m;
     m.sc = reinterpret_cast<C*>(smem + 2 * S::buf_bytes);
     m.sd = reinterpret_cast<T*>(m.sc + B);
     m.sla = reinterpret_cast<int*>(m.sd + 4 * B);
@@ -249,7 +252,7 @@ __global__ void __launch_bounds__(kOutThreads, OuterMinBlocks<T>::value)
 #pragma unroll
     for (int k = 0; k < 4; ++k)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) acc[k][i] = C{0, 0};
+        for (int i = 0; i < 4; ++i) acc[k][i] = vzero<C>();
 
     // this warp's runs: lz whose stencil [lz, lz + w) meets [z0, z0 + 4), and the
     // y-classes meeting its half: {0, 1} for the lower, {1, 2} for the upper rows
@@ -257,14 +260,14 @@ __global__ void __launch_bounds__(kOutThreads, OuterMinBlocks<T>::value)
     const int c_lo = h, c_hi = h + 1;
 
     const int nbatch = (int)((end - beg + B - 1) / B);
-    produce<T, W, kOutThreads, 0>(threadIdx.x, p, c, beg, (int)min((uint32_t)B, end - beg),
+    produce<T, V, W, kOutThreads, 0>(threadIdx.x, p, c, beg, (int)min((uint32_t)B, end - beg),
                                   reinterpret_cast<T*>(smem), goff0, m, beta);
     __syncthreads();
     for (int kb = 0; kb < nbatch; ++kb) {
         OUTER_PROF_T(t0);
         if (producer && kb + 1 < nbatch) {
             const uint32_t p1 = beg + (uint32_t)(kb + 1) * B;
-            produce<T, W, kProducers, 1>(ptid, p, c, p1, (int)min((uint32_t)B, end - p1),
+            produce<T, V, W, kProducers, 1>(ptid, p, c, p1, (int)min((uint32_t)B, end - p1),
                                          reinterpret_cast<T*>(smem + ((kb + 1) & 1) * S::buf_bytes),
                                          goff0 + ((kb + 1) & 1) * kGoffStride, m, beta);
         }
@@ -283,12 +286,9 @@ __global__ void __launch_bounds__(kOutThreads, OuterMinBlocks<T>::value)
                 Vec4<T>::load(wz, swz + j * E + z0);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    const T zr = bxv.x * wz[k], zi = bxv.y * wz[k];
+                    const C z = vscale(bxv, wz[k]);
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        acc[k][i].x = fma(zr, wy[i], acc[k][i].x);
-                        acc[k][i].y = fma(zi, wy[i], acc[k][i].y);
-                    }
+                    for (int i = 0; i < 4; ++i) vfma(acc[k][i], z, wy[i]);
                 }
             }
         }
@@ -305,10 +305,13 @@ __global__ void __launch_bounds__(kOutThreads, OuterMinBlocks<T>::value)
     for (int k = 0; k < 4; ++k)
 #pragma unroll
         for (int i = 0; i < 4; ++i) tile[((z0 + k) * E + y0 + i) * P + tx.shift + x] = acc[k][i];
-    if constexpr (P > E) {  // fp32: zero the two pad columns outside the shifted window
+    if constexpr (P > E) {  // zero the P - E pad columns outside the shifted window
         const int rr = threadIdx.x;  // E*E == kOutThreads rows
-        tile[rr * P + (tx.shift ? 0 : E)] = C{0, 0};
-        tile[rr * P + E + 1] = C{0, 0};
+#pragma unroll
+        for (int q = 0; q < P - E; ++q) {
+            const int col = q < tx.shift ? q : E + q;
+            tile[rr * P + col] = vzero<C>();
+        }
     }
     fence_proxy_async_smem();
     __syncthreads();
@@ -334,12 +337,11 @@ __global__ void __launch_bounds__(kOutThreads, OuterMinBlocks<T>::value)
 #endif
 }
 
-template <typename T, int W>
-cudaError_t launch_outer_w(const Geom& g, const PtsView<T>& p, int64_t nbins,
-                           const typename Cx<T>::type* c, typename Cx<T>::type* grid,
-                           double beta, cudaStream_t s) {
-    const size_t smem = OuterSmem<T, W>::bytes();
-    auto kern = spread_outer_kernel<T, W>;
+template <typename T, typename V, int W>
+cudaError_t launch_outer_w(const Geom& g, const PtsView<T>& p, int64_t nbins, const V* c,
+                           V* grid, double beta, cudaStream_t s) {
+    const size_t smem = OuterSmem<T, V, W>::bytes();
+    auto kern = spread_outer_kernel<T, V, W>;
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) {
@@ -360,25 +362,24 @@ bool spread_outer_applies(const Geom& g) {
 template <typename T>
 size_t spread_outer_smem_bytes(const Geom& g) {
     switch (g.w) {
-        case 2: return OuterSmem<T, 2>::bytes();   case 3: return OuterSmem<T, 3>::bytes();
-        case 4: return OuterSmem<T, 4>::bytes();   case 5: return OuterSmem<T, 5>::bytes();
-        case 6: return OuterSmem<T, 6>::bytes();   case 7: return OuterSmem<T, 7>::bytes();
-        case 8: return OuterSmem<T, 8>::bytes();   case 9: return OuterSmem<T, 9>::bytes();
-        case 10: return OuterSmem<T, 10>::bytes(); case 11: return OuterSmem<T, 11>::bytes();
-        case 12: return OuterSmem<T, 12>::bytes();
+#define NUFFT_OS(WW) OuterSmem<T, typename Cx<T>::type, WW>::bytes()
+        case 2: return NUFFT_OS(2);   case 3: return NUFFT_OS(3);   case 4: return NUFFT_OS(4);
+        case 5: return NUFFT_OS(5);   case 6: return NUFFT_OS(6);   case 7: return NUFFT_OS(7);
+        case 8: return NUFFT_OS(8);   case 9: return NUFFT_OS(9);   case 10: return NUFFT_OS(10);
+        case 11: return NUFFT_OS(11); case 12: return NUFFT_OS(12);
+#undef NUFFT_OS
         default: return 0;
     }
 }
 
-template <typename T>
-cudaError_t launch_spread_outer(const Geom& g, const PtsView<T>& p, int64_t nbins,
-                                const typename Cx<T>::type* c, typename Cx<T>::type* grid,
-                                double beta, cudaStream_t s) {
+template <typename T, typename V>
+cudaError_t launch_outer_v(const Geom& g, const PtsView<T>& p, int64_t nbins, const V* c,
+                           V* grid, double beta, cudaStream_t s) {
     if (!spread_outer_applies(g)) return cudaErrorNotSupported;
     switch (g.w) {
 #define NUFFT_OW(WW) \
     case WW:         \
-        return launch_outer_w<T, WW>(g, p, nbins, c, grid, beta, s);
+        return launch_outer_w<T, V, WW>(g, p, nbins, c, grid, beta, s);
         NUFFT_OW(2) NUFFT_OW(3) NUFFT_OW(4) NUFFT_OW(5) NUFFT_OW(6) NUFFT_OW(7) NUFFT_OW(8)
         NUFFT_OW(9) NUFFT_OW(10) NUFFT_OW(11) NUFFT_OW(12)
 #undef NUFFT_OW
@@ -387,10 +388,27 @@ cudaError_t launch_spread_outer(const Geom& g, const PtsView<T>& p, int64_t nbin
     }
 }
 
+template <typename T>
+cudaError_t launch_spread_outer(const Geom& g, const PtsView<T>& p, int64_t nbins,
+                                const typename Cx<T>::type* c, typename Cx<T>::type* grid,
+                                double beta, cudaStream_t s) {
+    return launch_outer_v<T, typename Cx<T>::type>(g, p, nbins, c, grid, beta, s);
+}
+template <typename T>
+cudaError_t launch_spread_outer_real(const Geom& g, const PtsView<T>& p, int64_t nbins,
+                                     const T* c, T* grid, double beta, cudaStream_t s) {
+    return launch_outer_v<T, T>(g, p, nbins, c, grid, beta, s);
+}
+
 template cudaError_t launch_spread_outer<float>(const Geom&, const PtsView<float>&, int64_t,
                                                 const float2*, float2*, double, cudaStream_t);
 template cudaError_t launch_spread_outer<double>(const Geom&, const PtsView<double>&, int64_t,
                                                  const double2*, double2*, double, cudaStream_t);
+template cudaError_t launch_spread_outer_real<float>(const Geom&, const PtsView<float>&, int64_t,
+                                                     const float*, float*, double, cudaStream_t);
+template cudaError_t launch_spread_outer_real<double>(const Geom&, const PtsView<double>&, int64_t,
+                                                      const double*, double*, double,
+                                                      cudaStream_t);
 template size_t spread_outer_smem_bytes<float>(const Geom&);
 template size_t spread_outer_smem_bytes<double>(const Geom&);
 

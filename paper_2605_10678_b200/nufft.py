@@ -61,7 +61,8 @@ _EXPORTS = ["nufft_default_opts", "nufft_plan", "nufft_setpts", "nufft_execute_t
             "nufft_execute_type2", "nufft_spread", "nufft_interp", "nufft_destroy",
             "nufft_get_info", "nufft_strerror", "nufft_comm_unique_id", "nufft_comm_init",
             "nufft_comm_destroy", "nufft_local_modes", "nufft_pif_poisson", "nufft_pif_kick",
-            "nufft_pif_drift", "nufft_pif_migrate"]
+            "nufft_pif_drift", "nufft_pif_migrate", "nufft_execute_type1_real",
+            "nufft_execute_type2_real"]
 
 _lib = None
 
@@ -78,7 +79,8 @@ def lib():
         L.nufft_plan.argtypes = [ctypes.c_int64] * 3 + [ctypes.c_int, ctypes.c_double, ctypes.c_int,
                                                         ctypes.POINTER(Opts), ctypes.POINTER(vp)]
         L.nufft_setpts.argtypes = [vp, ctypes.c_int64, vp, vp, vp]
-        for f in ("nufft_execute_type1", "nufft_execute_type2", "nufft_spread", "nufft_interp"):
+        for f in ("nufft_execute_type1", "nufft_execute_type2", "nufft_spread", "nufft_interp",
+                  "nufft_execute_type1_real", "nufft_execute_type2_real"):
             getattr(L, f).argtypes = [vp, vp, vp]
         L.nufft_destroy.argtypes = [vp]
         L.nufft_get_info.argtypes = [vp, ctypes.POINTER(Info)]
@@ -258,6 +260,27 @@ class Plan:
         with torch.cuda.device(self.device):
             _check(lib().nufft_execute_type2(self._h, pf, pc), "nufft_execute_type2")
         return c
+
+    def type1_real(self, c: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Type 1 of REAL strengths (R2C path); returns the complex (Hermitian) modes."""
+        fk = self._out(out, self.local_shape, c)
+        pc = _ptr(c, self.real, self.Np, "c")
+        pf = _ptr(fk, self.cplx, math.prod(self.local_shape), "fk")
+        with torch.cuda.device(self.device):
+            _check(lib().nufft_execute_type1_real(self._h, pc, pf), "nufft_execute_type1_real")
+        return fk
+
+    def type2_real(self, fk: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Real part of type 2 (C2R path); returns Np reals."""
+        if out is None:
+            dev = self.device if fk.is_cuda else torch.device("cpu")
+            out = torch.empty((self.Np,), dtype=self.real, device=dev,
+                              pin_memory=(dev.type == "cpu" and torch.cuda.is_available()))
+        pf = _ptr(fk, self.cplx, math.prod(self.local_shape), "fk")
+        pc = _ptr(out, self.real, self.Np, "c")
+        with torch.cuda.device(self.device):
+            _check(lib().nufft_execute_type2_real(self._h, pf, pc), "nufft_execute_type2_real")
+        return out
 
     def spread(self, c: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         N1, N2, N3 = self.N
