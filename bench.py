@@ -189,14 +189,20 @@ def run_ours(args, cfg):
                    tile=args.tile, spread_warps=args.spread_warps, comm=comm)
     pts, c, fk = make_inputs(cfg, rank, ws, device, plan.local_modes() if ws > 1 else None)
     Np = pts[0].numel()
+    if args.real:  # real strengths / outputs: the R2C / C2R path
+        if ws > 1:
+            raise SystemExit("--real is single-GPU only")
+        c = c.real.contiguous()
     c2 = torch.empty(Np, dtype=c.dtype, device=device)
     fk_out = torch.empty_like(fk)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=device)
+    t1 = plan.type1_real if args.real else plan.type1
+    t2 = plan.type2_real if args.real else plan.type2
 
     def step():
         plan.setpts(*pts)
-        plan.type1(c, out=fk_out)
-        plan.type2(fk, out=c2)
+        t1(c, out=fk_out)
+        t2(fk, out=c2)
 
     for _ in range(args.warmup):
         step()
@@ -241,8 +247,8 @@ def run_ours(args, cfg):
 
     def e2e_step():
         plan.setpts(*hp)
-        plan.type1(hc, out=hfk_out)
-        plan.type2(hfk, out=hc2)
+        t1(hc, out=hfk_out)
+        t2(hfk, out=hc2)
 
     e2e_steps = max(3, min(args.steps, 20))
     for _ in range(2):
@@ -263,8 +269,9 @@ def run_ours(args, cfg):
         te = float(t.item())
     r = 8 if cfg["prec"] == "f64" else 4
     nmodes = fk.numel()  # this rank's mode block
-    h2d = 3 * Np * r + Np * 2 * r + nmodes * 2 * r
-    d2h = nmodes * 2 * r + Np * 2 * r
+    cr = 1 if args.real else 2  # reals per strength / output value
+    h2d = 3 * Np * r + Np * cr * r + nmodes * 2 * r
+    d2h = nmodes * 2 * r + Np * cr * r
     if ws > 1:  # whole-job bytes
         tot = torch.tensor([h2d, d2h], device=device, dtype=torch.float64)
         torch.distributed.all_reduce(tot)
@@ -291,6 +298,7 @@ def run_ours(args, cfg):
                        "N": list(N), "Np_total": Np_total, "eps": cfg["eps"],
                        "w": plan.info()["w"], "precision": cfg["prec"], "points": cfg["kind"],
                        "tile": plan.info()["tile"],
+                       "values": "real (R2C / C2R)" if args.real else "complex",
                        "parallelism": f"z-slab x{ws} (NCCL halos + all-to-all)" if ws > 1 else "1 GPU",
                        "l2": "flushed (512 MB write) before every timed step"},
             "stage_ms_median": med,
@@ -347,7 +355,8 @@ def run_pif(args, cfg):
     stream = torch.cuda.current_stream(device)
     comm = nb.Comm() if ws > 1 else None
     sim = LandauPIF(cfg["N"], cfg["Np"], eps=cfg["eps"], dt=cfg["dt"], precision=cfg["prec"],
-                    comm=comm, device=device, timing=True)
+                    comm=comm, device=device, timing=True, tile=args.tile,
+                    spread_warps=args.spread_warps)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=device)
     for _ in range(args.warmup):
         sim.step()
@@ -525,7 +534,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--tile", default=None, help="bin edge T or Tx,Ty,Tz (default: built-in table)")
-    ap.add_argument("--spread-warps", type=int, default=0, help="4 or 8 (default: built-in)")
+    ap.add_argument("--spread-warps", type=int, default=0,
+                    help="spread kernel: 1 rows, 2 outer products, 4 / 8 smem planes (default: built-in)")
+    ap.add_argument("--real", action="store_true",
+                    help="NUFFT configs: real strengths / outputs (R2C / C2R transforms)")
     args = ap.parse_args()
     if args.tile is not None:
         t = [int(v) for v in args.tile.split(",")]

@@ -181,6 +181,8 @@ int nufft_pif_poisson(nufft_handle h, const void* rho_k, void* ex_k, void* ey_k,
 /* Leapfrog kick of one velocity component: v[j] += scale * Re(e[j]), j < Np (e complex,
  * e.g. a type-2 output; scale = (q/m) dt / L^3). */
 int nufft_pif_kick(nufft_handle h, int64_t Np, void* v, const void* e, double scale);
+/* The same kick from a REAL field sample e (Np reals, e.g. a nufft_execute_type2_real output). */
+int nufft_pif_kick_real(nufft_handle h, int64_t Np, void* v, const void* e, double scale);
 /* Drift: x += v dt on each axis, folded onto [0, L). */
 int nufft_pif_drift(nufft_handle h, int64_t Np, void* x, void* y, void* z, const void* vx,
                     const void* vy, const void* vz, double dt);

@@ -51,12 +51,13 @@ __global__ void poisson_kernel(const typename Cx<T>::type* __restrict__ rho, int
     }
 }
 
+// v += s Re(e): e complex (stride 2, real parts) or real (stride 1, a type2_real output)
 template <typename T>
-__global__ void kick_kernel(int64_t Np, T* __restrict__ v,
-                            const typename Cx<T>::type* __restrict__ e, T s) {
+__global__ void kick_kernel(int64_t Np, T* __restrict__ v, const T* __restrict__ e, int stride,
+                            T s) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < Np;
          j += (int64_t)gridDim.x * blockDim.x)
-        v[j] += s * e[j].x;
+        v[j] += s * e[j * stride];
 }
 
 template <typename T>
@@ -95,7 +96,14 @@ cudaError_t launch_pif_poisson(const typename Cx<T>::type* rho, const int64_t N[
 template <typename T>
 cudaError_t launch_pif_kick(int64_t Np, T* v, const typename Cx<T>::type* e, double s,
                             cudaStream_t st) {
-    if (Np > 0) kick_kernel<T><<<grid1d(Np), kThreads, 0, st>>>(Np, v, e, (T)s);
+    if (Np > 0)
+        kick_kernel<T><<<grid1d(Np), kThreads, 0, st>>>(Np, v, reinterpret_cast<const T*>(e), 2,
+                                                        (T)s);
+    return cudaGetLastError();
+}
+template <typename T>
+cudaError_t launch_pif_kick_real(int64_t Np, T* v, const T* e, double s, cudaStream_t st) {
+    if (Np > 0) kick_kernel<T><<<grid1d(Np), kThreads, 0, st>>>(Np, v, e, 1, (T)s);
     return cudaGetLastError();
 }
 
@@ -112,6 +120,7 @@ cudaError_t launch_pif_drift(int64_t Np, T* x, T* y, T* z, const T* vx, const T*
                                                const int64_t*, double, int, Cx<T>::type*,          \
                                                Cx<T>::type*, Cx<T>::type*, cudaStream_t);          \
     template cudaError_t launch_pif_kick<T>(int64_t, T*, const Cx<T>::type*, double, cudaStream_t); \
+    template cudaError_t launch_pif_kick_real<T>(int64_t, T*, const T*, double, cudaStream_t);      \
     template cudaError_t launch_pif_drift<T>(int64_t, T*, T*, T*, const T*, const T*, const T*,    \
                                              double, double, cudaStream_t);
 NUFFT_PIF_INST(float)

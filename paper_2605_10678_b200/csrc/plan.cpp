@@ -879,6 +879,19 @@ int nufft_pif_kick(nufft_handle p, int64_t Np, void* v, const void* e, double sc
     return NUFFT_OK;
 }
 
+int nufft_pif_kick_real(nufft_handle p, int64_t Np, void* v, const void* e, double scale) {
+    cudaGetLastError();
+    if (!p || Np < 0 || (Np > 0 && (!v || !e))) return NUFFT_ERR_ARG;
+    if (Np > 0 && (!is_device_ptr(v) || !is_device_ptr(e))) return NUFFT_ERR_ARG;
+    if (p->prec == NUFFT_F64)
+        NUFFT_CK(launch_pif_kick_real<double>(Np, static_cast<double*>(v),
+                                              static_cast<const double*>(e), scale, p->stream));
+    else
+        NUFFT_CK(launch_pif_kick_real<float>(Np, static_cast<float*>(v),
+                                             static_cast<const float*>(e), scale, p->stream));
+    return NUFFT_OK;
+}
+
 int nufft_pif_drift(nufft_handle p, int64_t Np, void* x, void* y, void* z, const void* vx,
                     const void* vy, const void* vz, double dt) {
     cudaGetLastError();

@@ -141,6 +141,8 @@ template <typename T>
 cudaError_t launch_pif_kick(int64_t Np, T* v, const typename Cx<T>::type* e, double s,
                             cudaStream_t st);
 template <typename T>
+cudaError_t launch_pif_kick_real(int64_t Np, T* v, const T* e, double s, cudaStream_t st);
+template <typename T>
 cudaError_t launch_pif_drift(int64_t Np, T* x, T* y, T* z, const T* vx, const T* vy, const T* vz,
                              double dt, double L, cudaStream_t s);
 

@@ -62,7 +62,7 @@ _EXPORTS = ["nufft_default_opts", "nufft_plan", "nufft_setpts", "nufft_execute_t
             "nufft_get_info", "nufft_strerror", "nufft_comm_unique_id", "nufft_comm_init",
             "nufft_comm_destroy", "nufft_local_modes", "nufft_pif_poisson", "nufft_pif_kick",
             "nufft_pif_drift", "nufft_pif_migrate", "nufft_execute_type1_real",
-            "nufft_execute_type2_real"]
+            "nufft_execute_type2_real", "nufft_pif_kick_real"]
 
 _lib = None
 
@@ -92,6 +92,7 @@ def lib():
         L.nufft_comm_destroy.argtypes = [vp]
         L.nufft_pif_poisson.argtypes = [vp, vp, vp, vp, vp]
         L.nufft_pif_kick.argtypes = [vp, ctypes.c_int64, vp, vp, ctypes.c_double]
+        L.nufft_pif_kick_real.argtypes = [vp, ctypes.c_int64, vp, vp, ctypes.c_double]
         L.nufft_pif_drift.argtypes = [vp, ctypes.c_int64, vp, vp, vp, vp, vp, vp, ctypes.c_double]
         L.nufft_pif_migrate.argtypes = [vp, ctypes.POINTER(ctypes.c_int64), ctypes.c_int64,
                                         vp, vp, vp, vp, vp, vp]

@@ -28,14 +28,16 @@ from . import nufft as _n
 
 class LandauPIF:
     def __init__(self, N, Np, eps=1e-4, dt=0.01, alpha=0.05, k=0.5, precision="f64",
-                 comm=None, device=None, seed=1, timing=False):
+                 comm=None, device=None, seed=1, timing=False, real=None, tile=None,
+                 spread_warps=0):
         import synthetic
         self.N = tuple(N)
         self.k, self.alpha, self.dt = k, alpha, dt
         self.L = 2 * math.pi / k
         self.qm = -1.0
         self.plan = _n.Plan(N, eps, precision=precision, L=self.L, comm=comm, device=device,
-                            timing=timing, points_owned=comm is not None)
+                            timing=timing, points_owned=comm is not None, tile=tile,
+                            spread_warps=spread_warps)
         dev = self.plan.device
         rdt, cdt = self.plan.real, self.plan.cplx
         self.Np_total = int(Np)
@@ -70,11 +72,16 @@ class LandauPIF:
                 self._state.append(buf)
             del a
         self.q = -self.L ** 3 / self.Np_total              # Q_e = -L^3 shared equally
-        self.charge = torch.full((self.cap,), self.q, dtype=cdt, device=dev)
+        # charges and fields are real: the real-valued transforms
+        # (R2C / C2R) are used on one GPU; slab plans use the complex transforms
+        self.real = (comm is None) if real is None else bool(real)
+        if self.real and comm is not None:
+            raise ValueError("real-valued transforms are single-GPU only")
+        self.charge = torch.full((self.cap,), self.q, dtype=rdt if self.real else cdt, device=dev)
         shape = self.plan.local_shape
         self.rho_k = torch.empty(shape, dtype=cdt, device=dev)
         self.e_k = [torch.empty(shape, dtype=cdt, device=dev) for _ in range(3)]
-        self.e_pts = torch.empty(self.cap, dtype=cdt, device=dev)
+        self.e_pts = torch.empty(self.cap, dtype=rdt if self.real else cdt, device=dev)
         self.t = 0.0
         if comm is not None:
             self.migrate()   # sampling at a slab edge may round into the neighbour's cell
@@ -100,15 +107,22 @@ class LandauPIF:
         n = self.Np
         with torch.cuda.device(p.device):
             p.setpts(self.x, self.y, self.z)                                   # sort
-            p.type1(self.charge[:n], out=self.rho_k)                           # (1) scatter
+            if self.real:
+                p.type1_real(self.charge[:n], out=self.rho_k)                  # (1) scatter
+            else:
+                p.type1(self.charge[:n], out=self.rho_k)
             _n._check(L.nufft_pif_poisson(p._h, self.rho_k.data_ptr(), *(e.data_ptr() for e in self.e_k)),
                       "nufft_pif_poisson")                                      # (2) field solve
             s = self.qm * self.dt / self.L ** 3
             e_pts = self.e_pts[:n]
+            kick = L.nufft_pif_kick_real if self.real else L.nufft_pif_kick
             for e_k, v in zip(self.e_k, (self.vx, self.vy, self.vz)):
-                p.type2(e_k, out=e_pts)                                         # (3) gather
-                _n._check(L.nufft_pif_kick(p._h, n, ctypes.c_void_p(v.data_ptr()),
-                                           ctypes.c_void_p(e_pts.data_ptr()), ctypes.c_double(s)),
+                if self.real:
+                    p.type2_real(e_k, out=e_pts)                                # (3) gather
+                else:
+                    p.type2(e_k, out=e_pts)
+                _n._check(kick(p._h, n, ctypes.c_void_p(v.data_ptr()),
+                               ctypes.c_void_p(e_pts.data_ptr()), ctypes.c_double(s)),
                           "nufft_pif_kick")                                     # (4) push
             _n._check(L.nufft_pif_drift(p._h, n, *(ctypes.c_void_p(a.data_ptr()) for a in
                                                    (self.x, self.y, self.z, self.vx, self.vy, self.vz)),

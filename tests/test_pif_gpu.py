@@ -25,9 +25,11 @@ def pifmod():
     return pif
 
 
-def test_one_step_matches_cpu_reference(pifmod):
+@pytest.mark.parametrize("real", [True, False])
+def test_one_step_matches_cpu_reference(pifmod, real):
+    # real: charges / fields through the R2C / C2R transforms (the one-GPU default)
     N, Np, eps, dt = (8, 10, 12), 6000, 1e-9, 0.05
-    sim = pifmod.LandauPIF(N, Np, eps=eps, dt=dt)
+    sim = pifmod.LandauPIF(N, Np, eps=eps, dt=dt, real=real)
     L = sim.L
     x0, y0, z0, vx0, vy0, vz0 = (t.cpu().numpy().copy() for t in
                                  (sim.x, sim.y, sim.z, sim.vx, sim.vy, sim.vz))
