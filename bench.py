@@ -55,6 +55,15 @@ CONFIGS = {
                    kind="pif", dt=0.01),
 }
 OUR_KERNELS_PER_STEP = 9  # bin_count, 3 scan, scatter | spread, truncate_deconv | pad, interp
+
+
+def kernels_per_step(info, ws):
+    """Our kernel launches per setpts + type 1 + type 2 (cuFFT's own not counted):
+    bin_count, 3 scan phases, scatter, [weights] | spread, truncate_deconv | pad,
+    interp; a slab plan adds 2 halo adds and the x/y pack + unpad instead of the
+    single-GPU truncate / pad (z_deconv, z_pad take their places)."""
+    n = OUR_KERNELS_PER_STEP + (1 if info.get("weights_precomputed") else 0)
+    return n + (4 if ws > 1 else 0)
 REF_SAMPLE = 1 << 19
 
 
@@ -133,19 +142,28 @@ def dist_env():
 
 
 def make_inputs(cfg, rank, ws, device, mode_block=None):
-    """This rank's share of the workload: Np / ws points drawn uniformly (or Landau)
-    over the WHOLE domain with a rank-shifted seed -- so most start on the wrong
-    slab and setpts redistributes them -- and its block of the global modes."""
+    """This rank's share of the workload.  The global problem is the same at every N
+    (strong scaling): Np points (uniform or Landau, seed 1), strengths (seed 2) and
+    modes (seed 3).  With N > 1 ranks every rank keeps the points whose fine z-cell
+    lies in its slab -- particles partitioned like the grid -- and
+    its block of the modes; the plan is told so (opts.points_owned)."""
     import synthetic
     rdt = torch.float64 if cfg["prec"] == "f64" else torch.float32
     cdt = torch.complex128 if cfg["prec"] == "f64" else torch.complex64
-    Np = cfg["Np"] // ws + (1 if rank < cfg["Np"] % ws else 0)
-    seed_shift = 1000 * rank
+    Np = cfg["Np"]
     if cfg["kind"] == "landau":
-        pts = synthetic.landau_points(Np, seed=1 + seed_shift, device=device, dtype=rdt)
+        pts = synthetic.landau_points(Np, seed=1, device=device, dtype=rdt)
     else:
-        pts = synthetic.uniform_points(Np, seed=1 + seed_shift, device=device, dtype=rdt)
-    c = synthetic.strengths(Np, seed=2 + seed_shift, device=device, dtype=cdt)
+        pts = synthetic.uniform_points(Np, seed=1, device=device, dtype=rdt)
+    c = synthetic.strengths(Np, seed=2, device=device, dtype=cdt)
+    if ws > 1:
+        L = cfg.get("L", 2 * math.pi)
+        nf3 = 2 * cfg["N"][2]
+        # the library's owner rule: floor(z nf3 / L) (fp64, z in [0, L)) // (nf3 / ws)
+        cell = torch.floor(pts[2].double() * (nf3 / L)).clamp_(max=nf3 - 1)
+        mine = torch.div(cell, nf3 // ws, rounding_mode="floor") == rank
+        pts = tuple(p[mine].contiguous() for p in pts)
+        c = c[mine].contiguous()
     fk = synthetic.modes(*cfg["N"], seed=3, device=device, dtype=cdt)
     if mode_block is not None:
         lo, hi = mode_block
@@ -186,7 +204,8 @@ def run_ours(args, cfg):
     N, Np_total = cfg["N"], cfg["Np"]
     comm = nb.Comm() if ws > 1 else None   # z-slab plan over NCCL
     plan = nb.Plan(N, cfg["eps"], precision=cfg["prec"], timing=True, device=device,
-                   tile=args.tile, spread_warps=args.spread_warps, comm=comm)
+                   tile=args.tile, spread_warps=args.spread_warps, comm=comm,
+                   points_owned=ws > 1)
     pts, c, fk = make_inputs(cfg, rank, ws, device, plan.local_modes() if ws > 1 else None)
     Np = pts[0].numel()
     if args.real:  # real strengths / outputs: the R2C / C2R path
@@ -299,13 +318,14 @@ def run_ours(args, cfg):
                        "w": plan.info()["w"], "precision": cfg["prec"], "points": cfg["kind"],
                        "tile": plan.info()["tile"],
                        "values": "real (R2C / C2R)" if args.real else "complex",
-                       "parallelism": f"z-slab x{ws} (NCCL halos + all-to-all)" if ws > 1 else "1 GPU",
+                       "parallelism": (f"z-slab x{ws} (points owned by slab, NCCL halos + "
+                                       f"all-to-all)") if ws > 1 else "1 GPU",
                        "l2": "flushed (512 MB write) before every timed step"},
             "stage_ms_median": med,
             "e2e": {"value": Np_total / (te / e2e_steps / 1e3), "unit": "points/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": te / e2e_steps},
-            "gpu_launches": OUR_KERNELS_PER_STEP * args.steps,
+            "gpu_launches": kernels_per_step(plan.info(), ws) * args.steps,
             "roofline": {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": hbm,
                          "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm,
                          "traffic": load_traffic(args.config, dom),
