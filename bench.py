@@ -484,6 +484,7 @@ def pif_cpu_baseline():
           (2 * math.pi / L) * n[2][:, None, None]]
     kk = ks[0] ** 2 + ks[1] ** 2 + ks[2] ** 2
     inv = np.where(kk > 0, 1.0 / np.where(kk > 0, kk, 1.0), 0.0)
+    inv[0, :, :] = inv[:, 0, :] = inv[:, :, 0] = 0.0   # no field on the Nyquist planes (R15)
     for d in range(3):
         e = oracle.type2(x, y, z, -1j * ks[d] * rho * inv, eps, L=L)
         v[d] += -dt * e.real / L ** 3

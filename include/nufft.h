@@ -130,12 +130,17 @@ int nufft_execute_type2(nufft_handle h, const void* fk, void* c);
 /* Real-valued transforms ("all implementations support real and complex-valued inputs",
  * PAPER.md:198).  Same plan, same points; the spread / interp grid is REAL and the FFT
  * runs on its half spectrum (R2C / C2R), halving grid bytes, FFT work and FMAs.
- *   type1_real: c = Np REAL strengths; fk = N1 N2 N3 complex out (Hermitian: fk[-n] =
- *               conj fk[n]), identical in value to nufft_execute_type1 with c + 0i.
+ * One GPU (full mode layout, N1 N2 N3 as for the complex calls):
+ *   type1_real: c = Np REAL strengths; fk = N1 N2 N3 complex out, identical in value to
+ *               nufft_execute_type1 with c + 0i (Hermitian where n and -n are stored).
  *   type2_real: fk = N1 N2 N3 complex in; c = Np REAL out, c_j = Re(sum_n fk[n]
- *               exp(-iflag i (2 pi / L) n . x_j)) -- the real part of nufft_execute_type2
- *               (exact when fk is Hermitian, e.g. a Fourier-space field of a real field).
- * Single-GPU plans only (NUFFT_ERR_UNSUPPORTED on a slab plan for now). */
+ *               exp(-iflag i (2 pi / L) n . x_j)) -- the real part of nufft_execute_type2.
+ * Slab plan (HALF-SPECTRUM layout: x index i1 = k1 in [0, N1/2] (N1/2 + 1 values), the
+ * rank's y-block and all z as in nufft_local_modes, x fastest) -- nothing crosses ranks:
+ *   type1_real: fk holds the type-1 values at k1 = 0 .. N1/2 (k1 = N1/2 is the conjugate
+ *               partner of -N1/2; the k1 < 0 half is conj fk[-k]).
+ *   type2_real: fk is the k1 >= 0 half of a Hermitian spectrum; c_j = the sum over its
+ *               Hermitian completion (the k1 = 0 plane enters through its Hermitian part). */
 int nufft_execute_type1_real(nufft_handle h, const void* c, void* fk);
 int nufft_execute_type2_real(nufft_handle h, const void* fk, void* c);
 
@@ -178,6 +183,9 @@ int nufft_local_modes(nufft_handle h, int64_t lo[3], int64_t hi[3]);
 /* Gauss's law in Fourier space on this rank's mode block (nufft_local_modes layout):
  *   E_k = -i k rho_k / |k|^2, k = 2 pi n / L, E_0 = 0.  rho_k, ex_k, ey_k, ez_k: complex. */
 int nufft_pif_poisson(nufft_handle h, const void* rho_k, void* ex_k, void* ey_k, void* ez_k);
+/* The same on the mode layout of the plan's REAL transforms (the half spectrum on a slab
+ * plan, the full box on one GPU). */
+int nufft_pif_poisson_real(nufft_handle h, const void* rho_k, void* ex_k, void* ey_k, void* ez_k);
 /* Leapfrog kick of one velocity component: v[j] += scale * Re(e[j]), j < Np (e complex,
  * e.g. a type-2 output; scale = (q/m) dt / L^3). */
 int nufft_pif_kick(nufft_handle h, int64_t Np, void* v, const void* e, double scale);

@@ -72,6 +72,13 @@ struct DistState {
     void* rbuf = nullptr;  // receive staging, np_local elements
     size_t sbuf_bytes = 0, rbuf_bytes = 0;
 
+    // real transforms (half-spectrum modes): batched 2D R2C / C2R of the owned planes,
+    // 1D z transforms of the NY (N1/2 + 1) lines, half planes nzl x nf2 x (nf1/2 + 1)
+    cufftHandle fft2r = 0, fft2c = 0, fft1h = 0;
+    bool real_ok = false;
+    void* hbuf = nullptr;
+    size_t hbuf_bytes = 0;
+
     // PIF particle migration (nufft_pif_migrate)
     unsigned long long* d_mig = nullptr;  // [P] pack cursors, [2] hole / tail counters, [1] flag
     void* mig_send = nullptr;             // leavers, 6 values each
@@ -120,46 +127,46 @@ int alltoallv(DistState* d, const void* send, const std::vector<unsigned long lo
     return NUFFT_OK;
 }
 
+// Ghost planes of the slab grid whose cells hold K reals (K = 2: complex, 1: real).
 template <typename T>
-int halo_accumulate(nufft_plan_s* p) {
+int halo_accumulate(nufft_plan_s* p, void* grid0, int K) {
     using C = typename Cx<T>::type;
     DistState* d = p->dist;
-    C* g0 = static_cast<C*>(p->grid0);
+    T* g0 = static_cast<T*>(grid0);
     const int prev = (d->r + d->P - 1) % d->P, next = (d->r + 1) % d->P;
-    const size_t pl = (size_t)d->plane;
+    const size_t pl = (size_t)d->plane * K;  // reals per plane
     NCK(ncclGroupStart());
     // my lower halo (hlo planes below plane 0) belongs to prev's top owned planes
-    NCK(ncclSend(g0 - d->hlo * pl, 2 * d->hlo * pl, d->real_t, prev, d->nccl, p->stream));
-    NCK(ncclRecv(d->halo_a, 2 * d->hlo * pl, d->real_t, next, d->nccl, p->stream));
+    NCK(ncclSend(g0 - d->hlo * pl, d->hlo * pl, d->real_t, prev, d->nccl, p->stream));
+    NCK(ncclRecv(d->halo_a, d->hlo * pl, d->real_t, next, d->nccl, p->stream));
     // my upper halo (hhi planes above the slab) belongs to next's bottom owned planes
-    NCK(ncclSend(g0 + d->nzl * pl, 2 * d->hhi * pl, d->real_t, next, d->nccl, p->stream));
-    NCK(ncclRecv(d->halo_b, 2 * d->hhi * pl, d->real_t, prev, d->nccl, p->stream));
+    NCK(ncclSend(g0 + d->nzl * pl, d->hhi * pl, d->real_t, next, d->nccl, p->stream));
+    NCK(ncclRecv(d->halo_b, d->hhi * pl, d->real_t, prev, d->nccl, p->stream));
     NCK(ncclGroupEnd());
-    NUFFT_CK(launch_halo_add<T>((int64_t)(d->hlo * pl), g0 + (d->nzl - d->hlo) * pl,
+    // the adds run on complex pairs (plane sizes are even)
+    NUFFT_CK(launch_halo_add<T>((int64_t)(d->hlo * pl / 2),
+                                reinterpret_cast<C*>(g0 + (d->nzl - d->hlo) * pl),
                                 static_cast<const C*>(d->halo_a), p->stream));
-    NUFFT_CK(launch_halo_add<T>((int64_t)(d->hhi * pl), g0, static_cast<const C*>(d->halo_b),
-                                p->stream));
+    NUFFT_CK(launch_halo_add<T>((int64_t)(d->hhi * pl / 2), reinterpret_cast<C*>(g0),
+                                static_cast<const C*>(d->halo_b), p->stream));
     return NUFFT_OK;
 }
-
 template <typename T>
-int halo_fill(nufft_plan_s* p) {
-    using C = typename Cx<T>::type;
+int halo_fill(nufft_plan_s* p, void* grid0, int K) {
     DistState* d = p->dist;
-    C* g0 = static_cast<C*>(p->grid0);
+    T* g0 = static_cast<T*>(grid0);
     const int prev = (d->r + d->P - 1) % d->P, next = (d->r + 1) % d->P;
-    const size_t pl = (size_t)d->plane;
+    const size_t pl = (size_t)d->plane * K;
     NCK(ncclGroupStart());
     // my bottom hhi owned planes are prev's upper halo; next's bottom planes are mine
-    NCK(ncclSend(g0, 2 * d->hhi * pl, d->real_t, prev, d->nccl, p->stream));
-    NCK(ncclRecv(g0 + d->nzl * pl, 2 * d->hhi * pl, d->real_t, next, d->nccl, p->stream));
+    NCK(ncclSend(g0, d->hhi * pl, d->real_t, prev, d->nccl, p->stream));
+    NCK(ncclRecv(g0 + d->nzl * pl, d->hhi * pl, d->real_t, next, d->nccl, p->stream));
     // my top hlo owned planes are next's lower halo; prev's top planes fill my lower halo
-    NCK(ncclSend(g0 + (d->nzl - d->hlo) * pl, 2 * d->hlo * pl, d->real_t, next, d->nccl, p->stream));
-    NCK(ncclRecv(g0 - d->hlo * pl, 2 * d->hlo * pl, d->real_t, prev, d->nccl, p->stream));
+    NCK(ncclSend(g0 + (d->nzl - d->hlo) * pl, d->hlo * pl, d->real_t, next, d->nccl, p->stream));
+    NCK(ncclRecv(g0 - d->hlo * pl, d->hlo * pl, d->real_t, prev, d->nccl, p->stream));
     NCK(ncclGroupEnd());
     return NUFFT_OK;
 }
-
 int fft_exec(nufft_plan_s* p, cufftHandle h, void* data, int sign) {
     const int dir = sign < 0 ? CUFFT_FORWARD : CUFFT_INVERSE;
     cufftResult r;
@@ -180,7 +187,7 @@ int type1_t(nufft_plan_s* p, const void* c_local, void* fk_local) {
     if ((st = do_spread(p, c_local, p->grid0))) return st;                         // C
     {
         StageTimer tm(p, EV_COMM);
-        if ((st = halo_accumulate<T>(p))) return st;                               // halos
+        if ((st = halo_accumulate<T>(p, p->grid0, 2))) return st;                 // halos
     }
     {
         StageTimer tm(p, EV_FFT);
@@ -222,9 +229,133 @@ int type2_t(nufft_plan_s* p, const void* fk_local, void* c_local) {
     }
     {
         StageTimer tm(p, EV_COMM);
-        if ((st = halo_fill<T>(p))) return st;                                     // halos
+        if ((st = halo_fill<T>(p, p->grid0, 2))) return st;                       // halos
     }
     return do_interp(p, p->grid0, c_local);                                        // C^T
+}
+
+int ensure_real_dist(nufft_plan_s* p) {
+    DistState* d = p->dist;
+    if (d->real_ok) return NUFFT_OK;
+    const bool f64 = p->prec == NUFFT_F64;
+    const int nf1 = (int)p->nf[0], nf2 = (int)p->nf[1], hx = nf1 / 2 + 1;
+    int n2[2] = {nf2, nf1};
+    int rembed[2] = {nf2, nf1}, cembed[2] = {nf2, hx};
+    if (cufftPlanMany(&d->fft2r, 2, n2, rembed, 1, nf2 * nf1, cembed, 1, nf2 * hx,
+                      f64 ? CUFFT_D2Z : CUFFT_R2C, (int)d->nzl) != CUFFT_SUCCESS)
+        return NUFFT_ERR_CUFFT;
+    if (cufftPlanMany(&d->fft2c, 2, n2, cembed, 1, nf2 * hx, rembed, 1, nf2 * nf1,
+                      f64 ? CUFFT_Z2D : CUFFT_C2R, (int)d->nzl) != CUFFT_SUCCESS) {
+        cufftDestroy(d->fft2r);
+        return NUFFT_ERR_CUFFT;
+    }
+    const int S = (int)(d->NY * (p->N[0] / 2 + 1));
+    int n1[1] = {(int)p->nf[2]};
+    int emb[1] = {(int)p->nf[2]};
+    if (cufftPlanMany(&d->fft1h, 1, n1, emb, S, 1, emb, S, 1, f64 ? CUFFT_Z2Z : CUFFT_C2C, S) !=
+        CUFFT_SUCCESS) {
+        cufftDestroy(d->fft2r);
+        cufftDestroy(d->fft2c);
+        return NUFFT_ERR_CUFFT;
+    }
+    d->real_ok = true;
+    size_t ws = 0;
+    cufftGetSize(d->fft2r, &ws);
+    p->bytes += ws;
+    cufftGetSize(d->fft2c, &ws);
+    p->bytes += ws;
+    cufftGetSize(d->fft1h, &ws);
+    p->bytes += ws;
+    if (cufftSetStream(d->fft2r, p->stream) != CUFFT_SUCCESS ||
+        cufftSetStream(d->fft2c, p->stream) != CUFFT_SUCCESS ||
+        cufftSetStream(d->fft1h, p->stream) != CUFFT_SUCCESS)
+        return NUFFT_ERR_CUFFT;
+    return ensure(p, &d->hbuf, &d->hbuf_bytes,
+                  (size_t)(d->nzl * p->nf[1] * (p->nf[0] / 2 + 1)) * p->cplx_size);
+}
+
+// real slab grid: (hlo + nzl + hhi) planes of reals at d_grid, plane 0 after hlo
+template <typename T>
+T* real_grid0(nufft_plan_s* p) {
+    return static_cast<T*>(p->d_grid) + p->dist->hlo * p->dist->plane;
+}
+
+template <typename T>
+int type1_real_t(nufft_plan_s* p, const void* c_local, void* fk_local) {
+    using C = typename Cx<T>::type;
+    DistState* d = p->dist;
+    int st;
+    const size_t rg = (size_t)((d->hlo + d->nzl + d->hhi) * d->plane) * sizeof(T);
+    NUFFT_CK(cudaMemsetAsync(p->d_grid, 0, rg, p->stream));
+    T* g0 = real_grid0<T>(p);
+    if ((st = do_spread_real(p, c_local, g0))) return st;                          // C
+    {
+        StageTimer tm(p, EV_COMM);
+        if ((st = halo_accumulate<T>(p, g0, 1))) return st;                        // halos
+    }
+    const int64_t H1 = p->N[0] / 2 + 1;
+    {
+        StageTimer tm(p, EV_FFT);
+        const cufftResult r =
+            p->prec == NUFFT_F64
+                ? cufftExecD2Z(d->fft2r, reinterpret_cast<cufftDoubleReal*>(g0),
+                               static_cast<cufftDoubleComplex*>(d->hbuf))
+                : cufftExecR2C(d->fft2r, reinterpret_cast<cufftReal*>(g0),
+                               static_cast<cufftComplex*>(d->hbuf));                // F (x, y)
+        if (r != CUFFT_SUCCESS) return NUFFT_ERR_CUFFT;
+        NUFFT_CK(launch_xy_pack_half<T>(static_cast<const C*>(d->hbuf), p->nf, d->nzl, p->N, d->P,
+                                        p->modeord, static_cast<C*>(d->xbuf), p->stream));
+        NCK(ncclAlltoAll(d->xbuf, d->ybuf, 2 * (size_t)(d->nzl * d->NY * H1), d->real_t, d->nccl,
+                         p->stream));                                               // transpose
+        if ((st = fft_exec(p, d->fft1h, d->ybuf, -1))) return st;                   // F (z), sign -
+    }
+    StageTimer tm(p, EV_DECONV);
+    NUFFT_CK(launch_z_deconv_half<T>(static_cast<const C*>(d->ybuf), p->nf, p->N, d->NY, d->y0,
+                                     static_cast<const T*>(p->d_p[0]),
+                                     static_cast<const T*>(p->d_p[1]),
+                                     static_cast<const T*>(p->d_p[2]), p->modeord,
+                                     p->iflag > 0 ? 1 : 0, static_cast<C*>(fk_local),
+                                     p->stream));                                  // chi (z), D
+    return NUFFT_OK;
+}
+
+template <typename T>
+int type2_real_t(nufft_plan_s* p, const void* fk_local, void* c_local) {
+    using C = typename Cx<T>::type;
+    DistState* d = p->dist;
+    int st;
+    const int64_t H1 = p->N[0] / 2 + 1;
+    {
+        StageTimer tm(p, EV_PAD);
+        // type-2 sign -iflag; the C2R path applies +, so a - sign conjugates the input
+        NUFFT_CK(launch_z_pad_half<T>(static_cast<const C*>(fk_local), p->nf, p->N, d->NY, d->y0,
+                                      static_cast<const T*>(p->d_p[0]),
+                                      static_cast<const T*>(p->d_p[1]),
+                                      static_cast<const T*>(p->d_p[2]), p->modeord,
+                                      p->iflag > 0 ? 1 : 0, static_cast<C*>(d->ybuf),
+                                      p->stream));                                 // D, chi^T (z)
+    }
+    T* g0 = real_grid0<T>(p);
+    {
+        StageTimer tm(p, EV_FFT);
+        if ((st = fft_exec(p, d->fft1h, d->ybuf, +1))) return st;                   // F^-1 (z)
+        NCK(ncclAlltoAll(d->ybuf, d->xbuf, 2 * (size_t)(d->nzl * d->NY * H1), d->real_t, d->nccl,
+                         p->stream));                                               // transpose
+        NUFFT_CK(launch_xy_unpad_half<T>(static_cast<const C*>(d->xbuf), p->nf, d->nzl, p->N,
+                                         d->P, p->modeord, static_cast<C*>(d->hbuf), p->stream));
+        const cufftResult r =
+            p->prec == NUFFT_F64
+                ? cufftExecZ2D(d->fft2c, static_cast<cufftDoubleComplex*>(d->hbuf),
+                               reinterpret_cast<cufftDoubleReal*>(g0))
+                : cufftExecC2R(d->fft2c, static_cast<cufftComplex*>(d->hbuf),
+                               reinterpret_cast<cufftReal*>(g0));                  // F^-1 (x, y)
+        if (r != CUFFT_SUCCESS) return NUFFT_ERR_CUFFT;
+    }
+    {
+        StageTimer tm(p, EV_COMM);
+        if ((st = halo_fill<T>(p, g0, 1))) return st;                              // halos
+    }
+    return do_interp_real(p, g0, c_local);                                         // C^T
 }
 
 }  // namespace
@@ -451,11 +582,73 @@ int dist_type2(nufft_plan_s* p, const void* fk, void* c) {
     return finish_output(p, c, cd, c_bytes, staged);
 }
 
+int dist_type1_real(nufft_plan_s* p, const void* c, void* fk) {
+    DistState* d = p->dist;
+    int st;
+    if ((st = ensure_real_dist(p))) return st;
+    const int64_t npu = dist_user_np(p);
+    const size_t rs = p->real_size;
+    const void* cd = nullptr;
+    if ((st = input_view(p, c, (size_t)npu * rs, 0, (size_t)npu * rs, &cd))) return st;
+    const size_t fk_bytes = (size_t)((p->N[0] / 2 + 1) * d->NY * p->N[2]) * p->cplx_size;
+    void* fkd = nullptr;
+    bool staged = false;
+    if ((st = output_view(p, fk, fk_bytes, &fkd, &staged))) return st;
+    const void* c_local = cd;
+    if (d->redist) {  // strengths follow their points
+        StageTimer tm(p, EV_COMM);
+        NUFFT_CK(launch_pack_bytes(npu, (int)rs, cd, d->owner, d->rank_in, d->d_off, d->sbuf,
+                                   false, p->stream));
+        if ((st = alltoallv(d, d->sbuf, d->scount, d->soff, d->rbuf, d->rcount, d->roff, rs,
+                            p->stream)))
+            return st;
+        c_local = d->rbuf;
+    }
+    st = p->prec == NUFFT_F64 ? type1_real_t<double>(p, c_local, fkd)
+                              : type1_real_t<float>(p, c_local, fkd);
+    if (st) return st;
+    return finish_output(p, fk, fkd, fk_bytes, staged);
+}
+
+int dist_type2_real(nufft_plan_s* p, const void* fk, void* c) {
+    DistState* d = p->dist;
+    int st;
+    if ((st = ensure_real_dist(p))) return st;
+    const int64_t npu = dist_user_np(p);
+    const size_t rs = p->real_size;
+    const size_t fk_bytes = (size_t)((p->N[0] / 2 + 1) * d->NY * p->N[2]) * p->cplx_size;
+    const void* fkd = nullptr;
+    if ((st = input_view(p, fk, fk_bytes, 0, fk_bytes, &fkd))) return st;
+    const size_t c_bytes = (size_t)npu * rs;
+    void* cd = nullptr;
+    bool staged = false;
+    if ((st = output_view(p, c, c_bytes, &cd, &staged))) return st;
+    void* c_local = d->redist ? d->rbuf : cd;
+    st = p->prec == NUFFT_F64 ? type2_real_t<double>(p, fkd, c_local)
+                              : type2_real_t<float>(p, fkd, c_local);
+    if (st) return st;
+    if (d->redist) {  // results return to the caller's ranks and order
+        StageTimer tm(p, EV_COMM);
+        if ((st = alltoallv(d, d->rbuf, d->rcount, d->roff, d->sbuf, d->scount, d->soff, rs,
+                            p->stream)))
+            return st;
+        NUFFT_CK(launch_pack_bytes(npu, (int)rs, d->sbuf, d->owner, d->rank_in, d->d_off, cd,
+                                   true, p->stream));
+    }
+    return finish_output(p, c, cd, c_bytes, staged);
+}
+
 void dist_destroy(nufft_plan_s* p) {
     DistState* d = p->dist;
     if (!d) return;
     if (d->fft2_ok) cufftDestroy(d->fft2);
     if (d->fft1_ok) cufftDestroy(d->fft1);
+    if (d->real_ok) {
+        cufftDestroy(d->fft2r);
+        cufftDestroy(d->fft2c);
+        cufftDestroy(d->fft1h);
+    }
+    dev_free(p, &d->hbuf, 0);
     dev_free(p, &d->xbuf, 0);
     dev_free(p, &d->ybuf, 0);
     dev_free(p, &d->halo_a, 0);

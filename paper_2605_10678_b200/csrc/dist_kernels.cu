@@ -98,6 +98,10 @@ __global__ void halo_add_kernel(int64_t n, C* __restrict__ dst, const C* __restr
 __device__ __forceinline__ int64_t mode_of(int64_t i, int64_t N, int modeord) {
     return modeord == 0 ? i - N / 2 : (i < N / 2 ? i : i - N);
 }
+// signed mode -> storage index
+__device__ __forceinline__ int64_t index_of(int64_t n, int64_t N, int modeord) {
+    return modeord == 0 ? n + N / 2 : (n >= 0 ? n : n + N);
+}
 
 // send[q][z][ys][x] = G[z][m2][m1], x in [0, N1), y storage index i2 = q*NY + ys
 template <typename C>
@@ -180,6 +184,101 @@ __global__ void xy_unpad_kernel(const C* __restrict__ recv, int64_t nf1, int64_t
             v = recv[((q * nzl + z) * NY + ys) * N1 + i1];
         }
         G[t] = v;
+    }
+}
+
+// ---------------------------------------------------------------- real transforms (slab)
+// Half-spectrum mode layout of a slab plan's real transforms: x index i1 = k1 in
+// [0, N1/2] (H1 = N1/2 + 1 values), the rank's y-block, all z.
+// xy_pack_half: after the batched 2D R2C of the owned planes (H: nzl x nf2 x hx,
+// hx = nf1/2 + 1), keep k1 in [0, N1/2] and the retained y modes, laid out by the
+// destination rank of their y-block: send[q][z][ys][x].
+template <typename C>
+__global__ void xy_pack_half_kernel(const C* __restrict__ H, int64_t nf1, int64_t nf2,
+                                    int64_t nzl, int64_t N1, int64_t N2, int P, int modeord,
+                                    C* __restrict__ send) {
+    const int64_t NY = N2 / P, H1 = N1 / 2 + 1, hx = nf1 / 2 + 1;
+    const int64_t total = nzl * N2 * H1;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t x = t % H1;
+        const int64_t ys = (t / H1) % NY;
+        const int64_t z = (t / (H1 * NY)) % nzl;
+        const int64_t q = t / (H1 * NY * nzl);
+        const int64_t n2 = mode_of(q * NY + ys, N2, modeord);
+        const int64_t m2 = n2 < 0 ? n2 + nf2 : n2;
+        send[t] = H[(z * nf2 + m2) * hx + x];
+    }
+}
+// fk[i3][ys][x] = Z[m3][ys][x] p1 p2 p3 (conj first when the type-1 sign is +: a
+// real grid's + transform is the conjugate of its - transform)
+template <typename T, typename C>
+__global__ void z_deconv_half_kernel(const C* __restrict__ Z, int64_t nf3, int64_t N1,
+                                     int64_t NY, int64_t N2, int64_t N3, int64_t y0,
+                                     const T* __restrict__ p1, const T* __restrict__ p2,
+                                     const T* __restrict__ p3, int modeord, int conj,
+                                     C* __restrict__ fk) {
+    const int64_t H1 = N1 / 2 + 1;
+    const int64_t total = N3 * NY * H1;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t x = t % H1, ys = (t / H1) % NY, i3 = t / (H1 * NY);
+        const int64_t n2 = mode_of(y0 + ys, N2, modeord), n3 = mode_of(i3, N3, modeord);
+        const int64_t m3 = n3 < 0 ? n3 + nf3 : n3;
+        // p is even: p1(k1) = p1(-k1), stored for k in [-N1/2, N1/2)
+        const T s = p1[N1 / 2 - x] * p2[n2 + N2 / 2] * p3[n3 + N3 / 2];
+        const C v = Z[(m3 * NY + ys) * H1 + x];
+        fk[t] = C{v.x * s, (conj ? -v.y : v.y) * s};
+    }
+}
+// Z[m3][ys][x] = fk[i3][ys][x] p1 p2 p3 on retained m3, 0 elsewhere (conj first when
+// the type-2 sign is -: the C2R path applies +)
+template <typename T, typename C>
+__global__ void z_pad_half_kernel(const C* __restrict__ fk, int64_t nf3, int64_t N1, int64_t NY,
+                                  int64_t N2, int64_t N3, int64_t y0, const T* __restrict__ p1,
+                                  const T* __restrict__ p2, const T* __restrict__ p3,
+                                  int modeord, int conj, C* __restrict__ Z) {
+    const int64_t H1 = N1 / 2 + 1;
+    const int64_t total = nf3 * NY * H1;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t x = t % H1, ys = (t / H1) % NY, m3 = t / (H1 * NY);
+        C v{0, 0};
+        if (m3 < N3 / 2 || m3 >= nf3 - N3 / 2) {
+            const int64_t n3 = m3 < N3 / 2 ? m3 : m3 - nf3;
+            const int64_t i3 = modeord == 0 ? n3 + N3 / 2 : (n3 >= 0 ? n3 : n3 + N3);
+            const int64_t n2 = mode_of(y0 + ys, N2, modeord);
+            const T s = p1[N1 / 2 - x] * p2[n2 + N2 / 2] * p3[n3 + N3 / 2];
+            const C f = fk[(i3 * NY + ys) * H1 + x];
+            v = C{f.x * s, (conj ? -f.y : f.y) * s};
+        }
+        Z[t] = v;
+    }
+}
+// H[z][m2][m1] (half planes, hx = nf1/2 + 1) = recv[q][z][ys][x] on retained
+// (k1 <= N1/2, k2), 0 elsewhere; on the k1 = 0 line the Hermitian part
+// (X(k2) + conj X(-k2)) / 2, which the C2R transform requires
+template <typename C>
+__global__ void xy_unpad_half_kernel(const C* __restrict__ recv, int64_t nf1, int64_t nf2,
+                                     int64_t nzl, int64_t N1, int64_t N2, int P, int modeord,
+                                     C* __restrict__ H) {
+    const int64_t NY = N2 / P, H1 = N1 / 2 + 1, hx = nf1 / 2 + 1;
+    const int64_t total = nzl * nf2 * hx;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t m1 = t % hx, m2 = (t / hx) % nf2, z = t / (hx * nf2);
+        const int64_t k2 = m2 < nf2 / 2 ? m2 : m2 - nf2;
+        auto X = [&](int64_t kk2) -> C {  // retained value at (m1, kk2) of plane z
+            if (m1 >= H1 || kk2 < -N2 / 2 || kk2 >= N2 / 2) return C{0, 0};
+            const int64_t i2 = index_of(kk2, N2, modeord), q = i2 / NY, ys = i2 - q * NY;
+            return recv[((q * nzl + z) * NY + ys) * H1 + m1];
+        };
+        C v = X(k2);
+        if (m1 == 0) {
+            const C b = X(-k2);
+            v = C{(v.x + b.x) * 0.5f, (v.y - b.y) * 0.5f};
+        }
+        H[t] = v;
     }
 }
 
@@ -406,6 +505,45 @@ cudaError_t launch_migrate_move(int64_t n, int64_t nleave, int64_t nrecv, T* con
     return cudaGetLastError();
 }
 
+template <typename T>
+cudaError_t launch_xy_pack_half(const typename Cx<T>::type* H, const int64_t nf[3], int64_t nzl,
+                                const int64_t N[3], int P, int modeord,
+                                typename Cx<T>::type* send, cudaStream_t s) {
+    xy_pack_half_kernel<typename Cx<T>::type><<<grid1d(nzl * N[1] * (N[0] / 2 + 1)), kThreads, 0,
+                                                s>>>(H, nf[0], nf[1], nzl, N[0], N[1], P, modeord,
+                                                     send);
+    return cudaGetLastError();
+}
+template <typename T>
+cudaError_t launch_z_deconv_half(const typename Cx<T>::type* Z, const int64_t nf[3],
+                                 const int64_t N[3], int64_t NY, int64_t y0, const T* p1,
+                                 const T* p2, const T* p3, int modeord, int conj,
+                                 typename Cx<T>::type* fk, cudaStream_t s) {
+    z_deconv_half_kernel<T, typename Cx<T>::type><<<grid1d(N[2] * NY * (N[0] / 2 + 1)), kThreads,
+                                                    0, s>>>(Z, nf[2], N[0], NY, N[1], N[2], y0, p1,
+                                                            p2, p3, modeord, conj, fk);
+    return cudaGetLastError();
+}
+template <typename T>
+cudaError_t launch_z_pad_half(const typename Cx<T>::type* fk, const int64_t nf[3],
+                              const int64_t N[3], int64_t NY, int64_t y0, const T* p1, const T* p2,
+                              const T* p3, int modeord, int conj, typename Cx<T>::type* Z,
+                              cudaStream_t s) {
+    z_pad_half_kernel<T, typename Cx<T>::type><<<grid1d(nf[2] * NY * (N[0] / 2 + 1)), kThreads, 0,
+                                                 s>>>(fk, nf[2], N[0], NY, N[1], N[2], y0, p1, p2,
+                                                      p3, modeord, conj, Z);
+    return cudaGetLastError();
+}
+template <typename T>
+cudaError_t launch_xy_unpad_half(const typename Cx<T>::type* recv, const int64_t nf[3],
+                                 int64_t nzl, const int64_t N[3], int P, int modeord,
+                                 typename Cx<T>::type* H, cudaStream_t s) {
+    xy_unpad_half_kernel<typename Cx<T>::type><<<grid1d(nzl * nf[1] * (nf[0] / 2 + 1)), kThreads,
+                                                 0, s>>>(recv, nf[0], nf[1], nzl, N[0], N[1], P,
+                                                         modeord, H);
+    return cudaGetLastError();
+}
+
 #define NUFFT_DIST_INST(T)                                                                         \
     template cudaError_t launch_owner_count<T>(int64_t, const T*, double, double, int64_t, int,      \
                                                uint32_t*, uint32_t*, unsigned long long*,            \
@@ -424,6 +562,23 @@ cudaError_t launch_migrate_move(int64_t n, int64_t nleave, int64_t nrecv, T* con
                                             const int64_t*, int, int, Cx<T>::type*, cudaStream_t);
 NUFFT_DIST_INST(float)
 NUFFT_DIST_INST(double)
+#define NUFFT_DIST_HALF_INST(T)                                                                   \
+    template cudaError_t launch_xy_pack_half<T>(const Cx<T>::type*, const int64_t*, int64_t,      \
+                                                const int64_t*, int, int, Cx<T>::type*,          \
+                                                cudaStream_t);                                     \
+    template cudaError_t launch_z_deconv_half<T>(const Cx<T>::type*, const int64_t*,              \
+                                                 const int64_t*, int64_t, int64_t, const T*,      \
+                                                 const T*, const T*, int, int, Cx<T>::type*,      \
+                                                 cudaStream_t);                                    \
+    template cudaError_t launch_z_pad_half<T>(const Cx<T>::type*, const int64_t*, const int64_t*, \
+                                              int64_t, int64_t, const T*, const T*, const T*, int, \
+                                              int, Cx<T>::type*, cudaStream_t);                   \
+    template cudaError_t launch_xy_unpad_half<T>(const Cx<T>::type*, const int64_t*, int64_t,     \
+                                                 const int64_t*, int, int, Cx<T>::type*,          \
+                                                 cudaStream_t);
+NUFFT_DIST_HALF_INST(float)
+NUFFT_DIST_HALF_INST(double)
+#undef NUFFT_DIST_HALF_INST
 template cudaError_t launch_migrate_count<float>(int64_t, const float*, double, double, int64_t,
                                                  int, int, unsigned long long*, cudaStream_t);
 template cudaError_t launch_migrate_count<double>(int64_t, const double*, double, double, int64_t,

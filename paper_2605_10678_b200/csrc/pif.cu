@@ -2,7 +2,8 @@
 // §4): the Poisson solve in Fourier space and the leapfrog push.
 // Not hot; coalesced single passes.
 //
-//   poisson  E_k = -i k rho_k / |k|^2, k = 2 pi n / L, E_0 = 0 (Gauss's law
+//   poisson  E_k = -i k rho_k / |k|^2, k = 2 pi n / L, E_0 = 0, E = 0 on the Nyquist
+//            planes (reading R15) (Gauss's law
 //            i k . E_k = rho_k; the neutralising ion background cancels k = 0)
 //   kick     v_d += s Re(E_d(x_j)),   s = (q/m) dt / L^3  (E(x) = L^-3 sum_k E_k e^{ikx})
 //   drift    x += v dt, folded onto [0, L)
@@ -28,7 +29,7 @@ __device__ __forceinline__ int64_t mode_of(int64_t i, int64_t N, int modeord) {
 template <typename T>
 __global__ void poisson_kernel(const typename Cx<T>::type* __restrict__ rho, int64_t N1, int64_t N2,
                                int64_t N3, int64_t lo1, int64_t lo2, int64_t lo3, int64_t n1l,
-                               int64_t n2l, int64_t n3l, double kscale, int modeord,
+                               int64_t n2l, int64_t n3l, double kscale, int modeord, int xhalf,
                                typename Cx<T>::type* __restrict__ ex,
                                typename Cx<T>::type* __restrict__ ey,
                                typename Cx<T>::type* __restrict__ ez) {
@@ -37,10 +38,14 @@ __global__ void poisson_kernel(const typename Cx<T>::type* __restrict__ rho, int
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
          t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t a = t % n1l, b = (t / n1l) % n2l, cc = t / (n1l * n2l);
-        const double k1 = kscale * (double)mode_of(lo1 + a, N1, modeord);
-        const double k2 = kscale * (double)mode_of(lo2 + b, N2, modeord);
-        const double k3 = kscale * (double)mode_of(lo3 + cc, N3, modeord);
-        const double kk = k1 * k1 + k2 * k2 + k3 * k3;
+        // xhalf: half-spectrum layout of a slab plan's real transforms (x index = k1 >= 0)
+        const int64_t m1 = xhalf ? lo1 + a : mode_of(lo1 + a, N1, modeord);
+        const int64_t m2 = mode_of(lo2 + b, N2, modeord), m3 = mode_of(lo3 + cc, N3, modeord);
+        const double k1 = kscale * (double)m1, k2 = kscale * (double)m2, k3 = kscale * (double)m3;
+        // Nyquist planes (k_d = -N_d/2, or k1 = +N1/2 in the half layout) carry no field:
+        // a real field's odd derivative vanishes there (reading R15)
+        const bool nyq = (xhalf ? m1 == N1 / 2 : m1 == -N1 / 2) || m2 == -N2 / 2 || m3 == -N3 / 2;
+        const double kk = nyq ? 0.0 : k1 * k1 + k2 * k2 + k3 * k3;
         const C r = rho[t];
         // -i k rho / |k|^2 = (k / |k|^2) (Im rho, -Re rho)
         const double inv = kk > 0.0 ? 1.0 / kk : 0.0;
@@ -84,12 +89,12 @@ __global__ void drift_kernel(int64_t Np, T* __restrict__ x, T* __restrict__ y, T
 
 template <typename T>
 cudaError_t launch_pif_poisson(const typename Cx<T>::type* rho, const int64_t N[3],
-                               const int64_t lo[3], const int64_t hi[3], double L, int modeord,
+                               const int64_t lo[3], const int64_t hi[3], double L, int modeord, int xhalf,
                                typename Cx<T>::type* ex, typename Cx<T>::type* ey,
                                typename Cx<T>::type* ez, cudaStream_t s) {
     const int64_t n1 = hi[0] - lo[0], n2 = hi[1] - lo[1], n3 = hi[2] - lo[2];
     poisson_kernel<T><<<grid1d(n1 * n2 * n3), kThreads, 0, s>>>(
-        rho, N[0], N[1], N[2], lo[0], lo[1], lo[2], n1, n2, n3, 2.0 * M_PI / L, modeord, ex, ey, ez);
+        rho, N[0], N[1], N[2], lo[0], lo[1], lo[2], n1, n2, n3, 2.0 * M_PI / L, modeord, xhalf, ex, ey, ez);
     return cudaGetLastError();
 }
 
@@ -117,7 +122,7 @@ cudaError_t launch_pif_drift(int64_t Np, T* x, T* y, T* z, const T* vx, const T*
 
 #define NUFFT_PIF_INST(T)                                                                        \
     template cudaError_t launch_pif_poisson<T>(const Cx<T>::type*, const int64_t*, const int64_t*, \
-                                               const int64_t*, double, int, Cx<T>::type*,          \
+                                               const int64_t*, double, int, int, Cx<T>::type*,     \
                                                Cx<T>::type*, Cx<T>::type*, cudaStream_t);          \
     template cudaError_t launch_pif_kick<T>(int64_t, T*, const Cx<T>::type*, double, cudaStream_t); \
     template cudaError_t launch_pif_kick_real<T>(int64_t, T*, const T*, double, cudaStream_t);      \

@@ -643,7 +643,7 @@ int nufft_execute_type1_real(nufft_handle p, const void* c, void* fk) {
     if (!p || !fk) return NUFFT_ERR_ARG;
     if (p->Np < 0) return NUFFT_ERR_NOT_SET;
     if (!c && user_np(p) > 0) return NUFFT_ERR_ARG;
-    if (p->dist) return NUFFT_ERR_UNSUPPORTED;
+    if (p->dist) return dist_type1_real(p, c, fk);
     int st;
     if ((st = ensure_real_fft(p))) return st;
     const void* cd = nullptr;
@@ -690,7 +690,7 @@ int nufft_execute_type2_real(nufft_handle p, const void* fk, void* c) {
     if (!p || !fk) return NUFFT_ERR_ARG;
     if (p->Np < 0) return NUFFT_ERR_NOT_SET;
     if (!c && user_np(p) > 0) return NUFFT_ERR_ARG;
-    if (p->dist) return NUFFT_ERR_UNSUPPORTED;
+    if (p->dist) return dist_type2_real(p, fk, c);
     int st;
     if ((st = ensure_real_fft(p))) return st;
     const size_t fk_bytes = (size_t)(p->N[0] * p->N[1] * p->N[2]) * p->cplx_size;
@@ -846,24 +846,40 @@ int nufft_local_modes(nufft_handle p, int64_t lo[3], int64_t hi[3]) {
     return NUFFT_OK;
 }
 
-int nufft_pif_poisson(nufft_handle p, const void* rho_k, void* ex_k, void* ey_k, void* ez_k) {
+static int pif_poisson(nufft_handle p, const void* rho_k, void* ex_k, void* ey_k, void* ez_k,
+                       bool real_layout) {
     cudaGetLastError();
     if (!p || !rho_k || !ex_k || !ey_k || !ez_k) return NUFFT_ERR_ARG;
     if (!is_device_ptr(rho_k) || !is_device_ptr(ex_k) || !is_device_ptr(ey_k) || !is_device_ptr(ez_k))
         return NUFFT_ERR_ARG;
     int64_t lo[3], hi[3];
     nufft_local_modes(p, lo, hi);
+    // a slab plan's real transforms hold x modes k1 = 0 .. N1/2 (half spectrum)
+    const int xhalf = (real_layout && p->dist) ? 1 : 0;
+    if (xhalf) {
+        lo[0] = 0;
+        hi[0] = p->N[0] / 2 + 1;
+    }
     if (p->prec == NUFFT_F64)
         NUFFT_CK(launch_pif_poisson<double>(static_cast<const double2*>(rho_k), p->N, lo, hi,
-                                            p->geom.L, p->modeord, static_cast<double2*>(ex_k),
-                                            static_cast<double2*>(ey_k), static_cast<double2*>(ez_k),
-                                            p->stream));
+                                            p->geom.L, p->modeord, xhalf,
+                                            static_cast<double2*>(ex_k), static_cast<double2*>(ey_k),
+                                            static_cast<double2*>(ez_k), p->stream));
     else
         NUFFT_CK(launch_pif_poisson<float>(static_cast<const float2*>(rho_k), p->N, lo, hi,
-                                           p->geom.L, p->modeord, static_cast<float2*>(ex_k),
-                                           static_cast<float2*>(ey_k), static_cast<float2*>(ez_k),
-                                           p->stream));
+                                           p->geom.L, p->modeord, xhalf,
+                                           static_cast<float2*>(ex_k), static_cast<float2*>(ey_k),
+                                           static_cast<float2*>(ez_k), p->stream));
     return NUFFT_OK;
+}
+
+int nufft_pif_poisson(nufft_handle p, const void* rho_k, void* ex_k, void* ey_k, void* ez_k) {
+    return pif_poisson(p, rho_k, ex_k, ey_k, ez_k, false);
+}
+
+int nufft_pif_poisson_real(nufft_handle p, const void* rho_k, void* ex_k, void* ey_k,
+                           void* ez_k) {
+    return pif_poisson(p, rho_k, ex_k, ey_k, ez_k, true);
 }
 
 int nufft_pif_kick(nufft_handle p, int64_t Np, void* v, const void* e, double scale) {

@@ -121,12 +121,17 @@ int local_sort(nufft_plan_s* p, int64_t Np, const void* x, const void* y, const 
 // C: grid0 += C c (grid must be zeroed by the caller); C^T: c = C^T grid0
 int do_spread(nufft_plan_s* p, const void* c_dev, void* grid0);
 int do_interp(nufft_plan_s* p, const void* grid0, void* c_dev);
+// real-valued spread / interp (grid of reals)
+int do_spread_real(nufft_plan_s* p, const void* c_dev, void* grid);
+int do_interp_real(nufft_plan_s* p, const void* grid, void* c_dev);
 
 // dist.cpp: the z-slab plan
 int dist_init(nufft_plan_s* p);
 int dist_setpts(nufft_plan_s* p, int64_t Np, const void* x, const void* y, const void* z);
 int dist_type1(nufft_plan_s* p, const void* c, void* fk);
 int dist_type2(nufft_plan_s* p, const void* fk, void* c);
+int dist_type1_real(nufft_plan_s* p, const void* c, void* fk);  // half-spectrum modes
+int dist_type2_real(nufft_plan_s* p, const void* fk, void* c);
 void dist_destroy(nufft_plan_s* p);
 int dist_local_modes(nufft_plan_s* p, int64_t lo[3], int64_t hi[3]);
 int64_t dist_user_np(nufft_plan_s* p);  // points the caller passed (before redistribution)
@@ -135,7 +140,7 @@ int64_t dist_user_np(nufft_plan_s* p);  // points the caller passed (before redi
 template <typename T>
 cudaError_t launch_pif_poisson(const typename Cx<T>::type* rho, const int64_t N[3],
                                const int64_t lo[3], const int64_t hi[3], double L, int modeord,
-                               typename Cx<T>::type* ex, typename Cx<T>::type* ey,
+                               int xhalf, typename Cx<T>::type* ex, typename Cx<T>::type* ey,
                                typename Cx<T>::type* ez, cudaStream_t s);
 template <typename T>
 cudaError_t launch_pif_kick(int64_t Np, T* v, const typename Cx<T>::type* e, double s,
@@ -165,6 +170,25 @@ cudaError_t launch_migrate_move(int64_t n, int64_t nleave, int64_t nrecv, T* con
                                 T* send, const T* recv, int64_t* hole, int64_t* lo,
                                 int64_t* tail, unsigned long long* nlo_ntail, int phase,
                                 cudaStream_t s);
+// real transforms on a slab plan (half-spectrum mode layout, x index = k1 in [0, N1/2])
+template <typename T>
+cudaError_t launch_xy_pack_half(const typename Cx<T>::type* H, const int64_t nf[3], int64_t nzl,
+                                const int64_t N[3], int P, int modeord,
+                                typename Cx<T>::type* send, cudaStream_t s);
+template <typename T>
+cudaError_t launch_z_deconv_half(const typename Cx<T>::type* Z, const int64_t nf[3],
+                                 const int64_t N[3], int64_t NY, int64_t y0, const T* p1,
+                                 const T* p2, const T* p3, int modeord, int conj,
+                                 typename Cx<T>::type* fk, cudaStream_t s);
+template <typename T>
+cudaError_t launch_z_pad_half(const typename Cx<T>::type* fk, const int64_t nf[3],
+                              const int64_t N[3], int64_t NY, int64_t y0, const T* p1, const T* p2,
+                              const T* p3, int modeord, int conj, typename Cx<T>::type* Z,
+                              cudaStream_t s);
+template <typename T>
+cudaError_t launch_xy_unpad_half(const typename Cx<T>::type* recv, const int64_t nf[3],
+                                 int64_t nzl, const int64_t N[3], int P, int modeord,
+                                 typename Cx<T>::type* H, cudaStream_t s);
 cudaError_t launch_pack_bytes(int64_t Np, int elem_bytes, const void* src, const uint32_t* owner,
                               const uint32_t* rank_in, const unsigned long long* off, void* dst,
                               bool unpack, cudaStream_t s);

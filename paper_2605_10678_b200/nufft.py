@@ -62,7 +62,7 @@ _EXPORTS = ["nufft_default_opts", "nufft_plan", "nufft_setpts", "nufft_execute_t
             "nufft_get_info", "nufft_strerror", "nufft_comm_unique_id", "nufft_comm_init",
             "nufft_comm_destroy", "nufft_local_modes", "nufft_pif_poisson", "nufft_pif_kick",
             "nufft_pif_drift", "nufft_pif_migrate", "nufft_execute_type1_real",
-            "nufft_execute_type2_real", "nufft_pif_kick_real"]
+            "nufft_execute_type2_real", "nufft_pif_kick_real", "nufft_pif_poisson_real"]
 
 _lib = None
 
@@ -91,6 +91,7 @@ def lib():
                                       ctypes.POINTER(vp)]
         L.nufft_comm_destroy.argtypes = [vp]
         L.nufft_pif_poisson.argtypes = [vp, vp, vp, vp, vp]
+        L.nufft_pif_poisson_real.argtypes = [vp, vp, vp, vp, vp]
         L.nufft_pif_kick.argtypes = [vp, ctypes.c_int64, vp, vp, ctypes.c_double]
         L.nufft_pif_kick_real.argtypes = [vp, ctypes.c_int64, vp, vp, ctypes.c_double]
         L.nufft_pif_drift.argtypes = [vp, ctypes.c_int64, vp, vp, vp, vp, vp, vp, ctypes.c_double]
@@ -200,6 +201,9 @@ class Plan:
         self.modes_lo, self.modes_hi = tuple(lo), tuple(hi)
         # this rank's mode block, (z, y, x) storage order, x fastest
         self.local_shape = tuple(hi[d] - lo[d] for d in (2, 1, 0))
+        # real transforms: the same on one GPU; the k1 = 0 .. N1/2 half on a slab plan
+        self.local_shape_real = (self.local_shape if comm is None else
+                                 self.local_shape[:2] + (self.N[0] // 2 + 1,))
 
     def local_modes(self):
         """[lo, hi) storage-index ranges per axis (x, y, z) of this rank's modes."""
@@ -264,9 +268,9 @@ class Plan:
 
     def type1_real(self, c: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         """Type 1 of REAL strengths (R2C path); returns the complex (Hermitian) modes."""
-        fk = self._out(out, self.local_shape, c)
+        fk = self._out(out, self.local_shape_real, c)
         pc = _ptr(c, self.real, self.Np, "c")
-        pf = _ptr(fk, self.cplx, math.prod(self.local_shape), "fk")
+        pf = _ptr(fk, self.cplx, math.prod(self.local_shape_real), "fk")
         with torch.cuda.device(self.device):
             _check(lib().nufft_execute_type1_real(self._h, pc, pf), "nufft_execute_type1_real")
         return fk
@@ -277,7 +281,7 @@ class Plan:
             dev = self.device if fk.is_cuda else torch.device("cpu")
             out = torch.empty((self.Np,), dtype=self.real, device=dev,
                               pin_memory=(dev.type == "cpu" and torch.cuda.is_available()))
-        pf = _ptr(fk, self.cplx, math.prod(self.local_shape), "fk")
+        pf = _ptr(fk, self.cplx, math.prod(self.local_shape_real), "fk")
         pc = _ptr(out, self.real, self.Np, "c")
         with torch.cuda.device(self.device):
             _check(lib().nufft_execute_type2_real(self._h, pf, pc), "nufft_execute_type2_real")

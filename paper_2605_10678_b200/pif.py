@@ -73,12 +73,12 @@ class LandauPIF:
             del a
         self.q = -self.L ** 3 / self.Np_total              # Q_e = -L^3 shared equally
         # charges and fields are real: the real-valued transforms
-        # (R2C / C2R) are used on one GPU; slab plans use the complex transforms
-        self.real = (comm is None) if real is None else bool(real)
-        if self.real and comm is not None:
-            raise ValueError("real-valued transforms are single-GPU only")
+        # (R2C / C2R) by default -- on a slab plan their modes are the k1 = 0 .. N1/2
+        # half spectrum (nufft.h), which the Poisson solve handles mode by mode
+        self.real = True if real is None else bool(real)
+        self.half = self.real and comm is not None
         self.charge = torch.full((self.cap,), self.q, dtype=rdt if self.real else cdt, device=dev)
-        shape = self.plan.local_shape
+        shape = self.plan.local_shape_real if self.real else self.plan.local_shape
         self.rho_k = torch.empty(shape, dtype=cdt, device=dev)
         self.e_k = [torch.empty(shape, dtype=cdt, device=dev) for _ in range(3)]
         self.e_pts = torch.empty(self.cap, dtype=rdt if self.real else cdt, device=dev)
@@ -111,7 +111,8 @@ class LandauPIF:
                 p.type1_real(self.charge[:n], out=self.rho_k)                  # (1) scatter
             else:
                 p.type1(self.charge[:n], out=self.rho_k)
-            _n._check(L.nufft_pif_poisson(p._h, self.rho_k.data_ptr(), *(e.data_ptr() for e in self.e_k)),
+            poisson = L.nufft_pif_poisson_real if self.real else L.nufft_pif_poisson
+            _n._check(poisson(p._h, self.rho_k.data_ptr(), *(e.data_ptr() for e in self.e_k)),
                       "nufft_pif_poisson")                                      # (2) field solve
             s = self.qm * self.dt / self.L ** 3
             e_pts = self.e_pts[:n]
@@ -131,9 +132,22 @@ class LandauPIF:
                 self.migrate()                                                  # slab ownership
         self.t += self.dt
 
+    def _half_weights(self):
+        """sum over the full box = sum over k1 = 0 (x1) and 0 < k1 < N1/2 (x2, conjugate
+        partners); the k1 = N1/2 column stands for the box's -N1/2 modes (x1)"""
+        h = self.N[0] // 2 + 1
+        w = torch.full((h,), 2.0, dtype=torch.float64, device=self.plan.device)
+        w[0] = 1.0
+        w[-1] = 1.0
+        return w
+
     def field_energy(self) -> float:
         """0.5 int |E|^2 dx = 0.5 L^-3 sum_k |E_k|^2 (this rank's modes; all-reduce for a slab plan)."""
-        w = sum(float((e.abs() ** 2).sum()) for e in self.e_k) * 0.5 / self.L ** 3
+        if self.half:
+            wx = self._half_weights()
+            w = sum(float(((e.abs() ** 2).double() * wx).sum()) for e in self.e_k) * 0.5 / self.L ** 3
+        else:
+            w = sum(float((e.abs() ** 2).sum()) for e in self.e_k) * 0.5 / self.L ** 3
         if self.plan.comm is not None:
             import torch.distributed as dist
             t = torch.tensor([w], dtype=torch.float64, device=self.plan.device)
@@ -142,9 +156,15 @@ class LandauPIF:
         return w
 
     def mode_amplitude(self, n=(1, 0, 0)) -> float:
-        """|E_x|-component amplitude of one mode n (centered storage), summed over ranks."""
+        """|E_x|-component amplitude of one mode n, summed over ranks."""
         lo, hi = self.plan.local_modes()
-        idx = [n[d] + self.N[d] // 2 for d in range(3)]
+        if self.half:  # x index = k1 >= 0; |E(n)| = |E(-n)| for a real field
+            if n[0] < 0:
+                n = tuple(-v for v in n)
+            lo, hi = (0, lo[1], lo[2]), (self.N[0] // 2 + 1, hi[1], hi[2])
+            idx = [n[0], n[1] + self.N[1] // 2, n[2] + self.N[2] // 2]
+        else:
+            idx = [n[d] + self.N[d] // 2 for d in range(3)]
         val = 0.0
         if all(lo[d] <= idx[d] < hi[d] for d in range(3)):
             e = self.e_k[0][idx[2] - lo[2], idx[1] - lo[1], idx[0] - lo[0]]

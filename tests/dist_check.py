@@ -108,6 +108,71 @@ def run_case(comm, N, Np, eps, prec, owned, kind, L):
     return int(flag.item()) == 0
 
 
+def run_real_case(comm, N, Np, eps, prec, owned, L):
+    """Real-valued transforms on the slab plan (half-spectrum layout, nufft.h) against the
+    one-GPU real transforms on the same points."""
+    rank, P = dist.get_rank(), dist.get_world_size()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    rdt = torch.float64 if prec == "f64" else torch.float32
+    pts = [p.to(rdt) for p in synthetic.uniform_points(Np, L=L, seed=31)]
+    c = synthetic.strengths(Np, seed=32).real.contiguous().to(rdt)
+    nf3 = 2 * N[2]
+    if owned:
+        zz = pts[2].double()
+        s = (zz - L * torch.floor(zz / L)) * (nf3 / L)
+        s = torch.where(s >= nf3, s - nf3, s)
+        owner = torch.clamp(torch.floor(s).long(), max=nf3 - 1) // (nf3 // P)
+        mine = torch.nonzero(owner == rank).flatten()
+    else:
+        mine = torch.arange(rank, Np, P)
+    xl, yl, zl = (p[mine].contiguous().to(dev) for p in pts)
+    plan = nb.Plan(N, eps, precision=prec, L=L, comm=comm, points_owned=owned)
+    lo, hi = plan.local_modes()
+    plan.setpts(xl, yl, zl)
+    fh_loc = plan.type1_real(c[mine].contiguous().to(dev))          # (N3, NY, N1/2 + 1)
+    fh = gather_cat(fh_loc, dim=1).cpu().to(torch.complex128)        # (N3, N2, N1/2 + 1)
+    ref = nb.Plan(N, eps, precision=prec, L=L)
+    ref.setpts(*(p.to(dev) for p in pts))
+    ff = ref.type1_real(c.to(dev)).cpu().to(torch.complex128)       # (N3, N2, N1) centered
+    h1 = N[0] // 2
+    # k1 in [0, N1/2): stored at centered x index N1/2 + k1
+    e1 = oracle.rel_l2(fh[:, :, :h1].numpy(), ff[:, :, h1:].numpy())
+    # k1 = +N1/2: the conjugate of (-N1/2, -k2, -k3) where -k2, -k3 are stored
+    a = fh[1:, 1:, h1]                                   # k2, k3 in (-N/2, N/2)
+    b = torch.conj(torch.flip(ff[1:, 1:, 0], dims=(0, 1))).resolve_conj()
+    e1b = oracle.rel_l2(a.numpy(), b.numpy())
+    # type 2: the slab's own half spectrum with the unpaired planes zeroed, against the
+    # one-GPU real transform of its Hermitian completion
+    fz = fh.clone()
+    fz[:, :, h1] = 0
+    fz[0, :, :] = 0
+    fz[:, 0, :] = 0
+    full = torch.zeros((N[2], N[1], N[0]), dtype=torch.complex128)
+    full[:, :, h1:] = fz[:, :, :h1]                                      # k1 >= 0
+    mirror = torch.conj(torch.flip(fz[1:, 1:, 1:h1 + 1], dims=(0, 1, 2))).resolve_conj()  # -k, k1 > 0
+    full[1:, 1:, 1:h1] = mirror[:, :, 1:]                                # k1 = -N1/2+1 .. -1
+    cdt = torch.complex128 if prec == "f64" else torch.complex64
+    c2_loc = plan.type2_real(fz[:, lo[1]:hi[1], :].contiguous().to(cdt).to(dev))
+    c2_ref = ref.type2_real(full.to(cdt).to(dev)).cpu().double()
+    parts = [None] * P
+    dist.all_gather_object(parts, (mine.numpy(), c2_loc.cpu().double().numpy()))
+    c2_all = torch.empty(Np, dtype=torch.float64)
+    for idx, val in parts:
+        c2_all[torch.from_numpy(idx)] = torch.from_numpy(val)
+    e2 = float(torch.linalg.norm(c2_all - c2_ref) / torch.linalg.norm(c2_ref))
+    tol = 1e-12 if prec == "f64" else 1e-5
+    ok = e1 <= tol and e1b <= tol and e2 <= tol
+    if rank == 0:
+        print(f"P={P} N={N} Np={Np} eps={eps:g} {prec} owned={owned} REAL: type1 vs 1-GPU "
+              f"{e1:.2e} (k1=N1/2: {e1b:.2e}), type2 {e2:.2e}  {'OK' if ok else 'FAIL'}",
+              flush=True)
+    plan.close()
+    ref.close()
+    flag = torch.tensor([0 if ok else 1], device=dev)
+    dist.all_reduce(flag)
+    return int(flag.item()) == 0
+
+
 def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -121,6 +186,12 @@ def main():
         ((64, 64, 64), 300000, 1e-5, "f64", False, "uniform", 2 * math.pi),
     ]
     ok = all([run_case(comm, *cs) for cs in cases])
+    real_cases = [
+        ((32, 32, 32), 40000, 1e-9, "f64", True, 2 * math.pi),
+        ((16, 24, 32), 30000, 1e-6, "f64", False, 4 * math.pi),
+        ((32, 32, 32), 40000, 1e-5, "f32", True, 2 * math.pi),
+    ]
+    ok = all([run_real_case(comm, *cs) for cs in real_cases]) and ok
     comm.close()
     dist.destroy_process_group()
     sys.exit(0 if ok else 1)

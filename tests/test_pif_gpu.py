@@ -45,6 +45,10 @@ def test_one_step_matches_cpu_reference(pifmod, real):
     k3 = (2 * math.pi / L) * n[2][:, None, None]
     kk = k1 ** 2 + k2 ** 2 + k3 ** 2
     inv = np.where(kk > 0, 1.0 / np.where(kk > 0, kk, 1.0), 0.0)
+    # reading R15: no field on the Nyquist planes (storage index 0 on any axis)
+    inv[0, :, :] = 0.0
+    inv[:, 0, :] = 0.0
+    inv[:, :, 0] = 0.0
     ek = [-1j * kd * rho * inv for kd in (k1, k2, k3)]
     assert np.abs(sim.e_k[0].cpu().numpy()[N[2] // 2, N[1] // 2, N[0] // 2]) == 0.0   # E_0 = 0
     for d in range(3):
