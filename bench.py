@@ -181,6 +181,41 @@ def algorithmic_bytes(cfg, stage):
     raise ValueError(stage)
 
 
+def algorithmic_flops(cfg, w, real=False):
+    """Per launch of spread or interp: the tensor-product evaluation of the w^3 stencil
+    per point -- w^3 value x weight multiply-adds (4 flops complex, 2 real) plus the
+    2 w^2 + 2 w (complex) partial products of the separable weights."""
+    per = 4 * w ** 3 + 2 * w ** 2 + 2 * w
+    return cfg["Np"] * (per // 2 if real else per)
+
+
+def alu_peak_tflops(prec, sm_mhz=1965.0):
+    """FMA-pipe peak from unit counts and clocks (B200_PROFILING.md: 148 SMs, 1965 MHz):
+    fp32 128 FMA lanes/clk/SM, fp64 64 (2 flops per FMA)."""
+    lanes = 128 if prec == "f32" else 64
+    return 148 * lanes * 2 * sm_mhz * 1e6 / 1e12
+
+
+def roofline_obj(cfg, dom, dom_ms, ws, w, real, traffic):
+    """The dominant kernel against its binding roofline: the spread / interp are bound
+    by the FMA pipes and shared memory (profiles/README.md: FP64 pipe 59 % busy at C3,
+    fp32 issue 63 % at C2b, DRAM 4-5 %) -> bound "alu"; the north_star's HBM fraction
+    of the same launch is reported alongside."""
+    hbm, peak_src = peaks()
+    bytes_alg = algorithmic_bytes(cfg, dom) / ws
+    gbs = bytes_alg / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
+    flops = algorithmic_flops(cfg, w, real) / ws
+    tfs = flops / (dom_ms / 1e3) / 1e12 if dom_ms > 0 else 0.0
+    peak = alu_peak_tflops(cfg["prec"])
+    return {"kernel": dom, "bound": "alu", "achieved": tfs, "peak": peak, "unit": "TFLOP/s",
+            "frac": tfs / peak, "peak_source": "derived: 148 SM x FMA lanes x 2 x 1965 MHz "
+                                                  "(B200_PROFILING.md), DESIGN.md section 9",
+            "traffic": traffic, "algorithmic_flops_per_launch": flops,
+            "ms_per_launch": dom_ms,
+            "hbm": {"achieved": gbs, "peak": hbm, "peak_source": peak_src, "unit": "GB/s",
+                    "frac": gbs / hbm, "algorithmic_bytes_per_launch": bytes_alg}}
+
+
 def load_traffic(cfg_key, kernel):
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
@@ -300,9 +335,6 @@ def run_ours(args, cfg):
     med = {k: statistics.median(v) for k, v in stage.items() if v and min(v) >= 0}
     dom = "spread" if med.get("ms_spread", 0) >= med.get("ms_interp", 0) else "interp"
     dom_ms = med["ms_" + dom]
-    hbm, peak_src = peaks()
-    bytes_alg = algorithmic_bytes(cfg, dom) / ws   # this rank's share of the launch
-    achieved = bytes_alg / (dom_ms / 1e3) / 1e9
     out = None
     if rank == 0:
         cpu = cpu_baseline(cfg) if (ws == 1 and not args.no_cpu_baseline) else None
@@ -326,10 +358,8 @@ def run_ours(args, cfg):
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": te / e2e_steps},
             "gpu_launches": kernels_per_step(plan.info(), ws) * args.steps,
-            "roofline": {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": hbm,
-                         "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm,
-                         "traffic": load_traffic(args.config, dom),
-                         "algorithmic_bytes_per_launch": bytes_alg, "ms_per_launch": dom_ms},
+            "roofline": roofline_obj(cfg, dom, dom_ms, ws, plan.info()["w"], args.real,
+                                     load_traffic(args.config, dom)),
             "clocks": clocks,
             "cpu_baseline": cpu,
         }
@@ -429,9 +459,6 @@ def run_pif(args, cfg):
     # dominant kernel per step: spread once, interp three times
     sp, ip = med.get("ms_spread", 0.0), 3 * med.get("ms_interp", 0.0)
     dom, dom_ms = ("spread", sp) if sp >= ip else ("interp", med.get("ms_interp", 0.0))
-    hbm, peak_src = peaks()
-    bytes_alg = algorithmic_bytes(cfg, dom) / ws
-    achieved = bytes_alg / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
     out = None
     if rank == 0:
         N = cfg["N"]
@@ -452,11 +479,12 @@ def run_pif(args, cfg):
             "e2e": {"value": te / e2e_steps / 1e3, "unit": "s/step", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 8,
                     "note": "state resident on device; field-energy scalar read back per step"},
-            "gpu_launches": (OUR_KERNELS_PER_STEP + 2 * 2 + 2) * args.steps,
-            "roofline": {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": hbm,
-                         "peak_source": peak_src, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": load_traffic(args.config, dom),
-                         "algorithmic_bytes_per_launch": bytes_alg, "ms_per_launch": dom_ms},
+            # setpts 5 [+ weights] | spread, truncate | poisson | 3 x (pad, interp, kick) |
+            # drift; a slab plan adds 2 halo adds, the x/y pack / unpads and migration (6)
+            "gpu_launches": (18 + (1 if sim.plan.info().get("weights_precomputed") else 0)
+                             + (12 if ws > 1 else 0)) * args.steps,
+            "roofline": roofline_obj(cfg, dom, dom_ms, ws, sim.plan.info()["w"], sim.real,
+                                     load_traffic(args.config, dom)),
             "clocks": clocks,
             "cpu_baseline": cpu,
         }
