@@ -143,6 +143,13 @@ int nufft_execute_type2(nufft_handle h, const void* fk, void* c);
  *               Hermitian completion (the k1 = 0 plane enters through its Hermitian part). */
 int nufft_execute_type1_real(nufft_handle h, const void* c, void* fk);
 int nufft_execute_type2_real(nufft_handle h, const void* fk, void* c);
+/* Three real type-2 transforms on the same points at once (a vector field, e.g. the PIF
+ * E field): fk0, fk1, fk2 as for type2_real; c = Np 3-vectors of reals,
+ * interleaved (c[3j + d] = component d at point j).  The three C2R outputs are kept as
+ * three real fine grids and gathered together with ONE evaluation of each point's weights.
+ * DEVICE pointers only.  Single-GPU plans (NUFFT_ERR_UNSUPPORTED on a slab plan). */
+int nufft_execute_type2_real3(nufft_handle h, const void* fk0, const void* fk1, const void* fk2,
+                              void* c);
 
 /* The spreading operator alone (Step 1): grid = C c on the periodic
  * nf1 x nf2 x nf3 fine grid (overwritten).  Single-GPU plans only. */
@@ -189,6 +196,13 @@ int nufft_pif_poisson_real(nufft_handle h, const void* rho_k, void* ex_k, void* 
 /* Leapfrog kick of one velocity component: v[j] += scale * Re(e[j]), j < Np (e complex,
  * e.g. a type-2 output; scale = (q/m) dt / L^3). */
 int nufft_pif_kick(nufft_handle h, int64_t Np, void* v, const void* e, double scale);
+/* Field gather fused with the kick: v_d[j] += scale E_d(x_j) for
+ * d = x, y, z, where E_d = type2_real(e_k[d]) -- nufft_execute_type2_real3 whose output
+ * stage adds into the velocities (no field array).  Single-GPU plans.  Measured slower
+ * than three nufft_execute_type2_real + nufft_pif_kick_real at C4 on B200 (the three
+ * component tiles halve the resident CTAs), so the PIF driver does not use it by default. */
+int nufft_pif_gather_kick(nufft_handle h, const void* ex_k, const void* ey_k, const void* ez_k,
+                          void* vx, void* vy, void* vz, double scale);
 /* The same kick from a REAL field sample e (Np reals, e.g. a nufft_execute_type2_real output). */
 int nufft_pif_kick_real(nufft_handle h, int64_t Np, void* v, const void* e, double scale);
 /* Drift: x += v dt on each axis, folded onto [0, L). */

@@ -156,20 +156,26 @@ struct TileX {
     int len;    // cells per row copied to / from the grid
     int pitch;  // smem row stride in cells (>= len)
 };
+// cells per 16-byte alignment unit: 16 / gcd(cell bytes, 16) (1 for 16 / 32 B cells,
+// 2 for 8 / 24 B, 4 for 4 / 12 B)
+template <int CELL_BYTES> struct AlignCells {
+    static constexpr int g = (CELL_BYTES % 16 == 0) ? 16 : (CELL_BYTES % 8 == 0) ? 8 : (CELL_BYTES % 4 == 0) ? 4 : 1;
+    static constexpr int value = 16 / g;
+};
 template <int CELL_BYTES>
 __host__ __device__ __forceinline__ int tile_len(int T, int W) {
-    constexpr int A = CELL_BYTES >= 16 ? 1 : 16 / CELL_BYTES;
+    constexpr int A = AlignCells<CELL_BYTES>::value;
     return A == 1 ? T + W : ((T + W + (A - 1) + (A - 1)) / A) * A;
 }
 template <int CELL_BYTES>
 __host__ __device__ __forceinline__ int tile_pitch(int T, int W) {
     const int len = tile_len<CELL_BYTES>(T, W);
-    if (CELL_BYTES >= 16) return len;
+    if (CELL_BYTES != 4 && CELL_BYTES != 8) return len;
     return len <= 8 ? 8 : 16 * ((len - 8 + 15) / 16) + 8;
 }
 template <int CELL_BYTES>
 __device__ __forceinline__ TileX tile_x(int bx, int T, int W) {
-    constexpr int A = CELL_BYTES >= 16 ? 1 : 16 / CELL_BYTES;
+    constexpr int A = AlignCells<CELL_BYTES>::value;
     const int ox = bx * T - W / 2;
     TileX t;
     t.shift = ox & (A - 1);

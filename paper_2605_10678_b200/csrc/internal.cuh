@@ -98,6 +98,14 @@ cudaError_t launch_spread_real(const Geom& g, const PtsView<T>& p, int64_t nbins
 template <typename T>
 cudaError_t launch_interp_real(const Geom& g, const PtsView<T>& p, int64_t nbins, const T* grid,
                                T* c, double beta, cudaStream_t s);
+// three real fields (x, y, z components: grids gstride reals apart) -> Np 3-vectors
+template <typename T>
+cudaError_t launch_interp_vec3(const Geom& g, const PtsView<T>& p, int64_t nbins, const T* grid,
+                               int64_t gstride, T* c, double beta, cudaStream_t s);
+template <typename T>
+cudaError_t launch_interp_vec3_kick(const Geom& g, const PtsView<T>& p, int64_t nbins,
+                                    const T* grid, int64_t gstride, T* v0, T* v1, T* v2,
+                                    double scale, double beta, cudaStream_t s);
 template <typename T> size_t spread_smem_bytes(const Geom& g);
 // spread_rows.cu: register-row spread (default when w <= 12 and T = 16 - w on every axis)
 bool spread_rows_applies(const Geom& g);

@@ -47,26 +47,97 @@ struct InterpSmem {
     }
 };
 
-__device__ __forceinline__ float vre(float2 v) { return v.x; }
-__device__ __forceinline__ double vre(double2 v) { return v.x; }
-__device__ __forceinline__ float vre(float v) { return v; }
-__device__ __forceinline__ double vre(double v) { return v; }
-__device__ __forceinline__ float vim(float2 v) { return v.y; }
-__device__ __forceinline__ double vim(double2 v) { return v.y; }
-__device__ __forceinline__ float vim(float) { return 0.f; }
-__device__ __forceinline__ double vim(double) { return 0.0; }
-template <typename V, typename T> __device__ __forceinline__ V vmake(T re, T im);
-template <> __device__ __forceinline__ float2 vmake<float2, float>(float re, float im) { return float2{re, im}; }
-template <> __device__ __forceinline__ double2 vmake<double2, double>(double re, double im) { return double2{re, im}; }
-template <> __device__ __forceinline__ float vmake<float, float>(float re, float) { return re; }
-template <> __device__ __forceinline__ double vmake<double, double>(double re, double) { return re; }
+// Grid values with NC real components: complex (2), real (1), or a real 3-vector
+// (3: the three field components of the PIF gather, sharing one weight evaluation).
+template <typename T> struct Vec3 { T c[3]; };
+template <typename V> struct VT;
+template <> struct VT<float2> {
+    static constexpr int n = 2;
+    __device__ static float get(const float2& v, int k) { return k ? v.y : v.x; }
+    __device__ static float2 make(const float (&a)[2]) { return float2{a[0], a[1]}; }
+};
+template <> struct VT<double2> {
+    static constexpr int n = 2;
+    __device__ static double get(const double2& v, int k) { return k ? v.y : v.x; }
+    __device__ static double2 make(const double (&a)[2]) { return double2{a[0], a[1]}; }
+};
+template <> struct VT<float> {
+    static constexpr int n = 1;
+    __device__ static float get(const float& v, int) { return v; }
+    __device__ static float make(const float (&a)[1]) { return a[0]; }
+};
+template <> struct VT<double> {
+    static constexpr int n = 1;
+    __device__ static double get(const double& v, int) { return v; }
+    __device__ static double make(const double (&a)[1]) { return a[0]; }
+};
+template <typename T> struct VT<Vec3<T>> {
+    static constexpr int n = 3;
+    __device__ static T get(const Vec3<T>& v, int k) { return v.c[k]; }
+    __device__ static Vec3<T> make(const T (&a)[3]) { return Vec3<T>{{a[0], a[1], a[2]}}; }
+};
+// Grid / shared-memory layout per value type: one tile of V cells, or -- for the
+// 3-vector -- three component grids (SoA, gstride reals apart in HBM) staged into
+// three consecutive component tiles (cell = one real).
+template <typename V> struct Layout {
+    using Cell = V;
+    static constexpr int comps = 1;
+    __device__ static V load(const Cell* t, int o, int) { return t[o]; }
+};
+template <typename T> struct Layout<Vec3<T>> {
+    using Cell = T;
+    static constexpr int comps = 3;
+    __device__ static Vec3<T> load(const T* t, int o, int nc) {
+        return Vec3<T>{{t[o], t[o + nc], t[o + 2 * nc]}};
+    }
+};
 
-template <typename T, typename V, int W>
+// Output stage of the gather: store the value at the caller's index ...
+template <typename V> struct StoreOut {
+    V* out;
+    template <typename T, int NC>
+    __device__ void operator()(uint32_t pj, const T (&tot)[NC]) const { out[pj] = VT<V>::make(tot); }
+};
+// ... or, for the PIF field gather, fuse the leapfrog kick:
+// v_d[pj] += s E_d(x_pj) for the three components (no field array in HBM)
+template <typename T> struct KickOut {
+    T* v0;
+    T* v1;
+    T* v2;
+    T s;
+    template <int NC>
+    __device__ void operator()(uint32_t pj, const T (&tot)[NC]) const {
+        static_assert(NC == 3, "a 3-component gather");
+        v0[pj] += s * tot[0];
+        v1[pj] += s * tot[1];
+        v2[pj] += s * tot[2];
+    }
+};
+
+// Four per-lane partial sums (points j0 .. j0 + 3) -> the total of point
+// j0 + (lane & 16 ? 1 : 0) + (lane & 8 ? 2 : 0) on every lane: a transposing
+// butterfly (offsets 16, 8 split the 4 sums over lane octets, 4, 2, 1 finish).
+template <typename T>
+__device__ __forceinline__ T reduce4(const T (&v)[4], int lane) {
+    const bool h16 = lane & 16, h8 = lane & 8;
+    T r0 = h16 ? v[1] : v[0], r1 = h16 ? v[3] : v[2];
+    r0 += __shfl_xor_sync(0xffffffffu, h16 ? v[0] : v[1], 16);
+    r1 += __shfl_xor_sync(0xffffffffu, h16 ? v[2] : v[3], 16);
+    T rr = h8 ? r1 : r0;
+    rr += __shfl_xor_sync(0xffffffffu, h8 ? r0 : r1, 8);
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) rr += __shfl_xor_sync(0xffffffffu, rr, o);
+    return rr;
+}
+
+template <typename T, typename V, int W, typename Out>
 __global__ void __launch_bounds__(kInterpThreads, 2)
-    interp_tile_kernel(Geom g, PtsView<T> p, const V* __restrict__ grid, V* __restrict__ out,
-                       T beta) {
+    interp_tile_kernel(Geom g, PtsView<T> p, const typename Layout<V>::Cell* __restrict__ grid,
+                       int64_t gstride, Out out, T beta) {
     using C = V;
-    constexpr bool kReal = sizeof(V) == sizeof(T);
+    using Cell = typename Layout<V>::Cell;
+    constexpr int NCOMP = Layout<V>::comps;  // component tiles (3 for the SoA 3-vector)
+    constexpr int NC = VT<V>::n;  // real components per value
     constexpr bool kFlat = W <= 5;
     constexpr int NQ = kFlat ? (W * W + 31) / 32 : 1;
     constexpr int XS = W <= 8 ? 8 : 16, YS = 32 / XS, NPASS = (W + YS - 1) / YS;
@@ -79,20 +150,20 @@ __global__ void __launch_bounds__(kInterpThreads, 2)
     if (beg == end) return;
 
     const int bx = b % g.nb[0], by = (b / g.nb[0]) % g.nb[1], bz = b / (g.nb[0] * g.nb[1]);
-    const TileX tx = tile_x<sizeof(C)>(bx, g.T[0], W);
+    const TileX tx = tile_x<sizeof(Cell)>(bx, g.T[0], W);
     const int Ey = g.T[1] + W, Ez = g.T[2] + W;
     const int pitch = tx.pitch, plane = pitch * Ey, ncell = plane * Ez;
-    C* tile = reinterpret_cast<C*>(smem);
+    Cell* tile = reinterpret_cast<Cell*>(smem);  // NCOMP tiles of ncell cells
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    T* wb = reinterpret_cast<T*>(tile + ncell) + warp * 32 * WS;  // [32][WS] per warp
+    T* wb = reinterpret_cast<T*>(tile + NCOMP * ncell) + warp * 32 * WS;  // [32][WS] per warp
     uint64_t* bar = reinterpret_cast<uint64_t*>(
-        (reinterpret_cast<uintptr_t>(reinterpret_cast<T*>(tile + ncell) + NW * 32 * WS) + 15) &
+        (reinterpret_cast<uintptr_t>(reinterpret_cast<T*>(tile + NCOMP * ncell) + NW * 32 * WS) + 15) &
         ~(uintptr_t)15);
 
     // ---- stage the subgrid with bulk copies (one mbarrier transaction)
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
-        mbar_arrive_expect_tx(bar, (unsigned)(Ey * Ez * tx.len * sizeof(C)));
+        mbar_arrive_expect_tx(bar, (unsigned)(NCOMP * Ey * Ez * tx.len * sizeof(Cell)));
     }
     __syncthreads();
     {
@@ -107,10 +178,13 @@ __global__ void __launch_bounds__(kInterpThreads, 2)
             // valid row there (the transaction count stays one full subgrid)
             if (gz < -g.hz_lo) gz = 0;
             const int gy = wrap1(oy + cy, nfy);
-            const C* grow = grid + (int64_t)nfx * ((int64_t)gz * nfy + gy);
-            C* trow = tile + r * pitch;
-            for (int k = 0; k < nseg; ++k)
-                bulk_g2s(trow + ss[k], grow + sg[k], (unsigned)(sn[k] * sizeof(C)), bar);
+#pragma unroll
+            for (int cc = 0; cc < NCOMP; ++cc) {
+                const Cell* grow = grid + cc * gstride + (int64_t)nfx * ((int64_t)gz * nfy + gy);
+                Cell* trow = tile + cc * ncell + r * pitch;
+                for (int k = 0; k < nseg; ++k)
+                    bulk_g2s(trow + ss[k], grow + sg[k], (unsigned)(sn[k] * sizeof(Cell)), bar);
+            }
         }
     }
 
@@ -172,12 +246,12 @@ __global__ void __launch_bounds__(kInterpThreads, 2)
         // four points at a time: independent accumulations, then a transposing
         // butterfly (offsets 16, 8 split the 4 sums over lane octets, 4, 2, 1 finish)
         for (int j0 = 0; j0 < np; j0 += 4) {
-            T vr[4], vi[4];
+            T acc[NC][4];
 #pragma unroll
             for (int g4 = 0; g4 < 4; ++g4) {
                 const int j = j0 + g4;
-                vr[g4] = 0;
-                vi[g4] = 0;
+#pragma unroll
+                for (int q = 0; q < NC; ++q) acc[q][g4] = 0;
                 if (j < np) {
                     const int base = __shfl_sync(0xffffffffu, my_base, j);
                     const T* wj = wb + j * WS;
@@ -188,64 +262,54 @@ __global__ void __launch_bounds__(kInterpThreads, 2)
 #pragma unroll
                         for (int q = 0; q < NQ; ++q) {
                             if (qok[q]) {
-                                const C* col = tile + base + qoff[q];
-                                T sr = 0, si = 0;
+                                const int col = base + qoff[q];
+                                T sv[NC];
+#pragma unroll
+                                for (int m = 0; m < NC; ++m) sv[m] = 0;
 #pragma unroll
                                 for (int k = 0; k < W; ++k) {
-                                    const C v = col[k * plane];
-                                    sr += vre(v) * wz[k];
-                                    if constexpr (!kReal) si += vim(v) * wz[k];
+                                    const C v = Layout<V>::load(tile, col + k * plane, ncell);
+#pragma unroll
+                                    for (int m = 0; m < NC; ++m) sv[m] += VT<C>::get(v, m) * wz[k];
                                 }
                                 const T wxy = wj[qx[q]] * wj[W + qy[q]];
-                                vr[g4] += sr * wxy;
-                                if constexpr (!kReal) vi[g4] += si * wxy;
+#pragma unroll
+                                for (int m = 0; m < NC; ++m) acc[m][g4] += sv[m] * wxy;
                             }
                         }
                     } else {
-                        const C* col0 = tile + base + sx;
+                        const int col0 = base + sx;
 #pragma unroll
                         for (int ps = 0; ps < NPASS; ++ps) {
                             const int y = sy0 + YS * ps;
                             if (sx < W && y < W) {
-                                const C* col = col0 + y * pitch;
-                                T sr = 0, si = 0;
+                                const int col = col0 + y * pitch;
+                                T sv[NC];
+#pragma unroll
+                                for (int m = 0; m < NC; ++m) sv[m] = 0;
 #pragma unroll
                                 for (int k = 0; k < W; ++k) {
-                                    const C v = col[k * plane];
-                                    sr += vre(v) * wz[k];
-                                    if constexpr (!kReal) si += vim(v) * wz[k];
+                                    const C v = Layout<V>::load(tile, col + k * plane, ncell);
+#pragma unroll
+                                    for (int m = 0; m < NC; ++m) sv[m] += VT<C>::get(v, m) * wz[k];
                                 }
                                 const T wy = wj[W + y];
-                                vr[g4] += sr * wy;
-                                if constexpr (!kReal) vi[g4] += si * wy;
+#pragma unroll
+                                for (int m = 0; m < NC; ++m) acc[m][g4] += sv[m] * wy;
                             }
                         }
                         const T wx = sx < W ? wj[sx] : (T)0;
-                        vr[g4] *= wx;
-                        if constexpr (!kReal) vi[g4] *= wx;
+#pragma unroll
+                        for (int m = 0; m < NC; ++m) acc[m][g4] *= wx;
                     }
                 }
             }
-            const bool h16 = lane & 16, h8 = lane & 8;
-            T r0 = h16 ? vr[1] : vr[0], r1 = h16 ? vr[3] : vr[2];
-            r0 += __shfl_xor_sync(0xffffffffu, h16 ? vr[0] : vr[1], 16);
-            r1 += __shfl_xor_sync(0xffffffffu, h16 ? vr[2] : vr[3], 16);
-            T rr = h8 ? r1 : r0, ii = 0;
-            rr += __shfl_xor_sync(0xffffffffu, h8 ? r0 : r1, 8);
+            T tot[NC];
 #pragma unroll
-            for (int o = 4; o > 0; o >>= 1) rr += __shfl_xor_sync(0xffffffffu, rr, o);
-            if constexpr (!kReal) {
-                T i0 = h16 ? vi[1] : vi[0], i1 = h16 ? vi[3] : vi[2];
-                i0 += __shfl_xor_sync(0xffffffffu, h16 ? vi[0] : vi[1], 16);
-                i1 += __shfl_xor_sync(0xffffffffu, h16 ? vi[2] : vi[3], 16);
-                ii = h8 ? i1 : i0;
-                ii += __shfl_xor_sync(0xffffffffu, h8 ? i0 : i1, 8);
-#pragma unroll
-                for (int o = 4; o > 0; o >>= 1) ii += __shfl_xor_sync(0xffffffffu, ii, o);
-            }
-            const int j = j0 + (h16 ? 1 : 0) + (h8 ? 2 : 0);
+            for (int m = 0; m < NC; ++m) tot[m] = reduce4<T>(acc[m], lane);
+            const int j = j0 + ((lane & 16) ? 1 : 0) + ((lane & 8) ? 2 : 0);
             const uint32_t pj = __shfl_sync(0xffffffffu, my_perm, j & 31);
-            if ((lane & 7) == 0 && j < np) out[pj] = vmake<C, T>(rr, ii);
+            if ((lane & 7) == 0 && j < np) out(pj, tot);
         }
         __syncwarp();
     }
@@ -256,22 +320,25 @@ __global__ void __launch_bounds__(kInterpThreads, 2)
 
 template <typename T, typename V, int W>
 size_t smem_w(const Geom& g) {
-    return InterpSmem<T, V, W>::bytes(tile_pitch<sizeof(V)>(g.T[0], W) * (g.T[1] + W) *
+    using Cell = typename Layout<V>::Cell;
+    return InterpSmem<T, V, W>::bytes(tile_pitch<sizeof(Cell)>(g.T[0], W) * (g.T[1] + W) *
                                       (g.T[2] + W));
 }
 
-template <typename T, typename V, int W>
-cudaError_t launch_w(const Geom& g, const PtsView<T>& p, int64_t nbins, const V* grid, V* c,
-                     double beta, cudaStream_t s) {
+template <typename T, typename V, int W, typename Out = StoreOut<V>>
+cudaError_t launch_w(const Geom& g, const PtsView<T>& p, int64_t nbins,
+                     const typename Layout<V>::Cell* grid, Out c, double beta, cudaStream_t s,
+                     int64_t gstride = 0) {
     const size_t smem = smem_w<T, V, W>(g);
-    auto kern = interp_tile_kernel<T, V, W>;
+    auto kern = interp_tile_kernel<T, V, W, Out>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return e;
     }
-    if (nbins > 0) kern<<<(unsigned)nbins, kInterpThreads, smem, s>>>(g, p, grid, c, (T)beta);
+    if (nbins > 0)
+        kern<<<(unsigned)nbins, kInterpThreads, smem, s>>>(g, p, grid, gstride, c, (T)beta);
     return cudaGetLastError();
 }
 
@@ -291,7 +358,8 @@ template <typename T>
 cudaError_t launch_interp(const Geom& g, const PtsView<T>& p, int64_t nbins,
                           const typename Cx<T>::type* grid, typename Cx<T>::type* c, double beta,
                           cudaStream_t s) {
-#define CALL(WW) launch_w<T, typename Cx<T>::type, WW>(g, p, nbins, grid, c, beta, s)
+#define CALL(WW) \
+    launch_w<T, typename Cx<T>::type, WW>(g, p, nbins, grid, StoreOut<typename Cx<T>::type>{c}, beta, s)
     NUFFT_W_SWITCH(CALL)
 #undef CALL
     return cudaErrorInvalidValue;
@@ -300,7 +368,33 @@ cudaError_t launch_interp(const Geom& g, const PtsView<T>& p, int64_t nbins,
 template <typename T>
 cudaError_t launch_interp_real(const Geom& g, const PtsView<T>& p, int64_t nbins, const T* grid,
                                T* c, double beta, cudaStream_t s) {
-#define CALL(WW) launch_w<T, T, WW>(g, p, nbins, grid, c, beta, s)
+#define CALL(WW) launch_w<T, T, WW>(g, p, nbins, grid, StoreOut<T>{c}, beta, s)
+    NUFFT_W_SWITCH(CALL)
+#undef CALL
+    return cudaErrorInvalidValue;
+}
+
+// grid = three real grids nf1 nf2 nz (x fastest), gstride reals apart; out = Np
+// 3-vectors of reals (caller order)
+template <typename T>
+cudaError_t launch_interp_vec3(const Geom& g, const PtsView<T>& p, int64_t nbins, const T* grid,
+                               int64_t gstride, T* c, double beta, cudaStream_t s) {
+#define CALL(WW)                                                                          \
+    launch_w<T, Vec3<T>, WW>(g, p, nbins, grid,                                           \
+                             StoreOut<Vec3<T>>{reinterpret_cast<Vec3<T>*>(c)}, beta, s, gstride)
+    NUFFT_W_SWITCH(CALL)
+#undef CALL
+    return cudaErrorInvalidValue;
+}
+
+// the same gather with the PIF kick fused into its output: v_d += s E_d
+template <typename T>
+cudaError_t launch_interp_vec3_kick(const Geom& g, const PtsView<T>& p, int64_t nbins,
+                                    const T* grid, int64_t gstride, T* v0, T* v1, T* v2,
+                                    double scale, double beta, cudaStream_t s) {
+#define CALL(WW)                                                                          \
+    launch_w<T, Vec3<T>, WW>(g, p, nbins, grid, KickOut<T>{v0, v1, v2, (T)scale}, beta, s,   \
+                             gstride)
     NUFFT_W_SWITCH(CALL)
 #undef CALL
     return cudaErrorInvalidValue;
@@ -322,6 +416,17 @@ template cudaError_t launch_interp_real<float>(const Geom&, const PtsView<float>
                                                const float*, float*, double, cudaStream_t);
 template cudaError_t launch_interp_real<double>(const Geom&, const PtsView<double>&, int64_t,
                                                 const double*, double*, double, cudaStream_t);
+template cudaError_t launch_interp_vec3<float>(const Geom&, const PtsView<float>&, int64_t,
+                                               const float*, int64_t, float*, double, cudaStream_t);
+template cudaError_t launch_interp_vec3<double>(const Geom&, const PtsView<double>&, int64_t,
+                                                const double*, int64_t, double*, double,
+                                                cudaStream_t);
+template cudaError_t launch_interp_vec3_kick<float>(const Geom&, const PtsView<float>&, int64_t,
+                                                    const float*, int64_t, float*, float*, float*,
+                                                    double, double, cudaStream_t);
+template cudaError_t launch_interp_vec3_kick<double>(const Geom&, const PtsView<double>&, int64_t,
+                                                     const double*, int64_t, double*, double*,
+                                                     double*, double, double, cudaStream_t);
 template size_t interp_smem_bytes<float>(const Geom&);
 template size_t interp_smem_bytes<double>(const Geom&);
 

@@ -166,32 +166,51 @@ int local_sort(nufft_plan_s* p, int64_t Np, const void* xd, const void* yd, cons
     if (Np >= (int64_t)1 << 31) return NUFFT_ERR_NPTS;
     int st = NUFFT_OK;
     if (Np > p->cap) {
-        dev_free(p, (void**)&p->bin_of, 4 * p->cap);
-        dev_free(p, (void**)&p->rank_of, 4 * p->cap);
         dev_free(p, &p->rec, 32 * p->cap);
         p->cap = 0;
         // a slab plan's local count drifts step to step (migration): 6 % slack there
         const size_t n = (size_t)(p->dist ? Np + Np / 16 : Np);
-        st = dev_alloc(p, (void**)&p->bin_of, 4 * n);
-        if (!st) st = dev_alloc(p, (void**)&p->rank_of, 4 * n);
-        if (!st) st = dev_alloc(p, &p->rec, 32 * n);
-        if (st) {
+        if ((st = dev_alloc(p, &p->rec, 32 * n))) {
             p->Np = -1;
             return st;
         }
         p->cap = (int64_t)n;
     }
+    // bin / rank scratch (dead once the records are written): inside the grid buffer
+    // when it is large enough -- no grid is live during setpts -- else own buffers
+    uint32_t* bin_of;
+    uint32_t* rank_of;
+    if (p->grid_bytes >= 8 * (size_t)Np) {
+        bin_of = static_cast<uint32_t*>(p->d_grid);
+        rank_of = bin_of + Np;
+    } else {
+        if ((size_t)Np > p->scratch_cap) {
+            dev_free(p, (void**)&p->bin_of, 4 * p->scratch_cap);
+            dev_free(p, (void**)&p->rank_of, 4 * p->scratch_cap);
+            p->scratch_cap = 0;
+            const size_t n = (size_t)(p->dist ? Np + Np / 16 : Np);
+            st = dev_alloc(p, (void**)&p->bin_of, 4 * n);
+            if (!st) st = dev_alloc(p, (void**)&p->rank_of, 4 * n);
+            if (st) {
+                p->Np = -1;
+                return st;
+            }
+            p->scratch_cap = n;
+        }
+        bin_of = p->bin_of;
+        rank_of = p->rank_of;
+    }
     if (p->prec == NUFFT_F64)
         NUFFT_CK(launch_bin_sort<double>(p->geom, Np, static_cast<const double*>(xd),
                                          static_cast<const double*>(yd),
                                          static_cast<const double*>(zd), p->count, p->offset,
-                                         p->blocksum, p->bin_of, p->rank_of,
+                                         p->blocksum, bin_of, rank_of,
                                          static_cast<PtRec<double>*>(p->rec), p->nbins, p->stream));
     else
         NUFFT_CK(launch_bin_sort<float>(p->geom, Np, static_cast<const float*>(xd),
                                         static_cast<const float*>(yd),
                                         static_cast<const float*>(zd), p->count, p->offset,
-                                        p->blocksum, p->bin_of, p->rank_of,
+                                        p->blocksum, bin_of, rank_of,
                                         static_cast<PtRec<float>*>(p->rec), p->nbins, p->stream));
     p->Np = Np;
     // per-point ES weights, reused by every execute on these points
@@ -357,7 +376,21 @@ int default_tile(int w, int prec, int64_t nf) {
     return t;
 }
 
+int ensure_complex_fft(nufft_plan_s* p) {
+    if (p->fft_ok) return NUFFT_OK;
+    if (cufftPlan3d(&p->fft, (int)p->nf[2], (int)p->nf[1], (int)p->nf[0],
+                    p->prec == NUFFT_F64 ? CUFFT_Z2Z : CUFFT_C2C) != CUFFT_SUCCESS)
+        return NUFFT_ERR_CUFFT;
+    p->fft_ok = true;
+    size_t ws = 0;
+    cufftGetSize(p->fft, &ws);
+    p->bytes += ws;
+    return cufftSetStream(p->fft, p->stream) == CUFFT_SUCCESS ? NUFFT_OK : NUFFT_ERR_CUFFT;
+}
+
 int do_fft(nufft_plan_s* p, int sign) {
+    int st = ensure_complex_fft(p);
+    if (st) return st;
     StageTimer tm(p, EV_FFT);
     const int dir = sign < 0 ? CUFFT_FORWARD : CUFFT_INVERSE;
     cufftResult r;
@@ -371,6 +404,12 @@ int do_fft(nufft_plan_s* p, int sign) {
 }
 
 int64_t user_np(nufft_plan_s* p) { return p->dist ? dist_user_np(p) : p->Np; }
+
+// bytes of one complex fine grid nf1 nf2 nf3 (the caller's grid of nufft_spread /
+// nufft_interp; p->grid_bytes is the plan's grid buffer, which may be larger)
+size_t cgrid_bytes(const nufft_plan_s* p) {
+    return (size_t)(p->nf[0] * p->nf[1] * p->nf[2]) * p->cplx_size;
+}
 
 }  // namespace
 
@@ -526,18 +565,8 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
                         (size_t)(2 * p->nf[1] * p->nf[2]) * p->real_size;
         st = dev_alloc(p, &p->d_grid, p->grid_bytes);
         p->grid0 = p->d_grid;
-        if (!st) {
-            cufftResult r = cufftPlan3d(&p->fft, (int)p->nf[2], (int)p->nf[1], (int)p->nf[0],
-                                        precision == NUFFT_F64 ? CUFFT_Z2Z : CUFFT_C2C);
-            if (r != CUFFT_SUCCESS) st = NUFFT_ERR_CUFFT;
-            else {
-                p->fft_ok = true;
-                size_t ws = 0;
-                cufftGetSize(p->fft, &ws);
-                p->bytes += ws;
-                if (cufftSetStream(p->fft, p->stream) != CUFFT_SUCCESS) st = NUFFT_ERR_CUFFT;
-            }
-        }
+        // the complex 3D cuFFT plan (and its workspace) is created on the first complex
+        // execute: a plan used only through the real transforms never holds it
     }
     if (!st) st = dev_alloc(p, (void**)&p->count, sizeof(uint32_t) * (size_t)p->nbins);
     if (!st) st = dev_alloc(p, (void**)&p->offset, sizeof(uint32_t) * (size_t)(p->nbins + 1));
@@ -585,7 +614,7 @@ int nufft_execute_type1(nufft_handle p, const void* c, void* fk) {
     void* fkd = nullptr;
     bool staged = false;
     if ((st = output_view(p, fk, fk_bytes, &fkd, &staged))) return st;
-    NUFFT_CK(cudaMemsetAsync(p->d_grid, 0, p->grid_bytes, p->stream));
+    NUFFT_CK(cudaMemsetAsync(p->d_grid, 0, cgrid_bytes(p), p->stream));
     if ((st = do_spread(p, cd, p->grid0))) return st;                   // Step 1: C
     if ((st = do_fft(p, p->iflag))) return st;                          // Step 2: F
     {
@@ -730,6 +759,110 @@ int nufft_execute_type2_real(nufft_handle p, const void* fk, void* c) {
     return finish_output(p, c, cd, c_bytes, staged);
 }
 
+namespace {
+int64_t nf3_of(const nufft_plan_s* p) { return p->nf[0] * p->nf[1] * p->nf[2]; }
+// three real fields (PIF E field) as three consecutive real fine grids (SoA) in the
+// grid buffer, each filled by the plan's C2R transform
+int real3_fields(nufft_plan_s* p, const void* fk0, const void* fk1, const void* fk2) {
+    // the three fields + a half spectrum live in the grid buffer (grown once): no
+    // other grid is live during the gather
+    const size_t nf3 = (size_t)(p->nf[0] * p->nf[1] * p->nf[2]);
+    const size_t half = (size_t)((p->nf[0] / 2 + 1) * p->nf[1] * p->nf[2]) * p->cplx_size;
+    const size_t need = 3 * nf3 * p->real_size + half;
+    if (p->grid_bytes < need) {
+        dev_free(p, &p->d_grid, p->grid_bytes);
+        p->grid_bytes = 0;
+        p->grid0 = nullptr;
+        int st = dev_alloc(p, &p->d_grid, need);
+        if (st) return st;
+        p->grid_bytes = need;
+        p->grid0 = p->d_grid;
+    }
+    p->vgrid = p->d_grid;
+    void* half3 = static_cast<char*>(p->d_grid) + 3 * nf3 * p->real_size;
+    int st0;
+    if ((st0 = ensure_real_fft(p))) return st0;
+    const void* fks[3] = {fk0, fk1, fk2};
+    const int sign_plus = p->iflag < 0 ? 1 : 0;
+    for (int d = 0; d < 3; ++d) {
+        {
+            StageTimer tm(p, EV_PAD);
+            if (p->prec == NUFFT_F64)
+                NUFFT_CK(launch_pad_precorrect_c2r<double>(
+                    static_cast<const double2*>(fks[d]), p->N,
+                    static_cast<const double*>(p->d_p[0]), static_cast<const double*>(p->d_p[1]),
+                    static_cast<const double*>(p->d_p[2]), p->modeord, sign_plus, p->nf,
+                    static_cast<double2*>(half3), p->stream));
+            else
+                NUFFT_CK(launch_pad_precorrect_c2r<float>(
+                    static_cast<const float2*>(fks[d]), p->N,
+                    static_cast<const float*>(p->d_p[0]), static_cast<const float*>(p->d_p[1]),
+                    static_cast<const float*>(p->d_p[2]), p->modeord, sign_plus, p->nf,
+                    static_cast<float2*>(half3), p->stream));
+        }
+        StageTimer tm(p, EV_FFT);
+        const cufftResult r =
+            p->prec == NUFFT_F64
+                ? cufftExecZ2D(p->fft_c2r, static_cast<cufftDoubleComplex*>(half3),
+                               static_cast<cufftDoubleReal*>(p->vgrid) + d * nf3)
+                : cufftExecC2R(p->fft_c2r, static_cast<cufftComplex*>(half3),
+                               static_cast<cufftReal*>(p->vgrid) + d * nf3);
+        if (r != CUFFT_SUCCESS) return NUFFT_ERR_CUFFT;
+    }
+    return NUFFT_OK;
+}
+}  // namespace
+
+int nufft_execute_type2_real3(nufft_handle p, const void* fk0, const void* fk1, const void* fk2,
+                              void* c) {
+    cudaGetLastError();
+    if (!p || !fk0 || !fk1 || !fk2) return NUFFT_ERR_ARG;
+    if (p->Np < 0) return NUFFT_ERR_NOT_SET;
+    if (!c && p->Np > 0) return NUFFT_ERR_ARG;
+    if (p->dist) return NUFFT_ERR_UNSUPPORTED;
+    if (!is_device_ptr(fk0) || !is_device_ptr(fk1) || !is_device_ptr(fk2) ||
+        (p->Np > 0 && !is_device_ptr(c)))
+        return NUFFT_ERR_ARG;
+    int st;
+    if ((st = real3_fields(p, fk0, fk1, fk2))) return st;
+    StageTimer tm(p, EV_INTERP);
+    if (p->prec == NUFFT_F64)
+        NUFFT_CK(launch_interp_vec3<double>(p->geom, pts_view<double>(p), p->nbins,
+                                            static_cast<const double*>(p->vgrid), nf3_of(p),
+                                            static_cast<double*>(c), p->beta, p->stream));
+    else
+        NUFFT_CK(launch_interp_vec3<float>(p->geom, pts_view<float>(p), p->nbins,
+                                           static_cast<const float*>(p->vgrid), nf3_of(p),
+                                           static_cast<float*>(c), p->beta, p->stream));
+    return NUFFT_OK;
+}
+
+int nufft_pif_gather_kick(nufft_handle p, const void* ex_k, const void* ey_k, const void* ez_k,
+                          void* vx, void* vy, void* vz, double scale) {
+    cudaGetLastError();
+    if (!p || !ex_k || !ey_k || !ez_k) return NUFFT_ERR_ARG;
+    if (p->Np < 0) return NUFFT_ERR_NOT_SET;
+    if (p->Np > 0 && (!vx || !vy || !vz)) return NUFFT_ERR_ARG;
+    if (p->dist) return NUFFT_ERR_UNSUPPORTED;
+    if (!is_device_ptr(ex_k) || !is_device_ptr(ey_k) || !is_device_ptr(ez_k) ||
+        (p->Np > 0 && (!is_device_ptr(vx) || !is_device_ptr(vy) || !is_device_ptr(vz))))
+        return NUFFT_ERR_ARG;
+    int st;
+    if ((st = real3_fields(p, ex_k, ey_k, ez_k))) return st;
+    StageTimer tm(p, EV_INTERP);
+    if (p->prec == NUFFT_F64)
+        NUFFT_CK(launch_interp_vec3_kick<double>(
+            p->geom, pts_view<double>(p), p->nbins, static_cast<const double*>(p->vgrid),
+            nf3_of(p), static_cast<double*>(vx), static_cast<double*>(vy), static_cast<double*>(vz), scale,
+            p->beta, p->stream));
+    else
+        NUFFT_CK(launch_interp_vec3_kick<float>(
+            p->geom, pts_view<float>(p), p->nbins, static_cast<const float*>(p->vgrid),
+            nf3_of(p), static_cast<float*>(vx), static_cast<float*>(vy), static_cast<float*>(vz), scale,
+            p->beta, p->stream));
+    return NUFFT_OK;
+}
+
 int nufft_spread(nufft_handle p, const void* c, void* grid) {
     cudaGetLastError();  // a stale non-sticky error of another caller is not ours
     if (!p || !grid || (!c && p->Np > 0)) return NUFFT_ERR_ARG;
@@ -741,10 +874,10 @@ int nufft_spread(nufft_handle p, const void* c, void* grid) {
         return st;
     void* gd = nullptr;
     bool staged = false;
-    if ((st = output_view(p, grid, p->grid_bytes, &gd, &staged))) return st;
-    NUFFT_CK(cudaMemsetAsync(gd, 0, p->grid_bytes, p->stream));
+    if ((st = output_view(p, grid, cgrid_bytes(p), &gd, &staged))) return st;
+    NUFFT_CK(cudaMemsetAsync(gd, 0, cgrid_bytes(p), p->stream));
     if ((st = do_spread(p, cd, gd))) return st;
-    return finish_output(p, grid, gd, p->grid_bytes, staged);
+    return finish_output(p, grid, gd, cgrid_bytes(p), staged);
 }
 
 int nufft_interp(nufft_handle p, const void* grid, void* c) {
@@ -754,7 +887,7 @@ int nufft_interp(nufft_handle p, const void* grid, void* c) {
     if (p->Np < 0) return NUFFT_ERR_NOT_SET;
     int st;
     const void* gd = nullptr;
-    if ((st = input_view(p, grid, p->grid_bytes, 0, p->grid_bytes, &gd))) return st;
+    if ((st = input_view(p, grid, cgrid_bytes(p), 0, cgrid_bytes(p), &gd))) return st;
     const size_t c_bytes = (size_t)p->Np * p->cplx_size;
     void* cd = nullptr;
     bool staged = false;

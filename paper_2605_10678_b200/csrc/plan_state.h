@@ -40,6 +40,8 @@ struct nufft_plan_s {
     // real grid is d_grid[0, nf^3) reals, the half spectrum follows it
     cufftHandle fft_r2c = 0, fft_c2r = 0;
     bool fft_r_ok = false;
+    // three real fields, SoA (nufft_execute_type2_real3 / nufft_pif_gather_kick)
+    void* vgrid = nullptr;  // = d_grid (grown to 3 fields + half spectrum)
 
     // points (this rank's, after redistribution)
     int64_t Np = -1;
@@ -47,8 +49,9 @@ struct nufft_plan_s {
     uint32_t* count = nullptr;
     uint32_t* offset = nullptr;
     uint32_t* blocksum = nullptr;
-    uint32_t* bin_of = nullptr;
+    uint32_t* bin_of = nullptr;   // setpts scratch when the grid buffer cannot host it
     uint32_t* rank_of = nullptr;
+    size_t scratch_cap = 0;
     void* rec = nullptr;  // Np sorted 32-byte records (PtRec)
     // per-point ES weights (opts.precompute): Np x 3w reals in sorted order
     int precompute = 0;     // opts value: 0 auto, 1 always, -1 never

@@ -62,7 +62,8 @@ _EXPORTS = ["nufft_default_opts", "nufft_plan", "nufft_setpts", "nufft_execute_t
             "nufft_get_info", "nufft_strerror", "nufft_comm_unique_id", "nufft_comm_init",
             "nufft_comm_destroy", "nufft_local_modes", "nufft_pif_poisson", "nufft_pif_kick",
             "nufft_pif_drift", "nufft_pif_migrate", "nufft_execute_type1_real",
-            "nufft_execute_type2_real", "nufft_pif_kick_real", "nufft_pif_poisson_real"]
+            "nufft_execute_type2_real", "nufft_pif_kick_real", "nufft_pif_poisson_real",
+            "nufft_execute_type2_real3", "nufft_pif_gather_kick"]
 
 _lib = None
 
@@ -92,6 +93,8 @@ def lib():
         L.nufft_comm_destroy.argtypes = [vp]
         L.nufft_pif_poisson.argtypes = [vp, vp, vp, vp, vp]
         L.nufft_pif_poisson_real.argtypes = [vp, vp, vp, vp, vp]
+        L.nufft_execute_type2_real3.argtypes = [vp, vp, vp, vp, vp]
+        L.nufft_pif_gather_kick.argtypes = [vp, vp, vp, vp, vp, vp, vp, ctypes.c_double]
         L.nufft_pif_kick.argtypes = [vp, ctypes.c_int64, vp, vp, ctypes.c_double]
         L.nufft_pif_kick_real.argtypes = [vp, ctypes.c_int64, vp, vp, ctypes.c_double]
         L.nufft_pif_drift.argtypes = [vp, ctypes.c_int64, vp, vp, vp, vp, vp, vp, ctypes.c_double]
@@ -285,6 +288,18 @@ class Plan:
         pc = _ptr(out, self.real, self.Np, "c")
         with torch.cuda.device(self.device):
             _check(lib().nufft_execute_type2_real(self._h, pf, pc), "nufft_execute_type2_real")
+        return out
+
+    def type2_real3(self, fk0, fk1, fk2, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Three real type-2 transforms at once (one weight evaluation per point);
+        returns (Np, 3) reals."""
+        if out is None:
+            out = torch.empty((self.Np, 3), dtype=self.real, device=self.device)
+        n = math.prod(self.local_shape_real)
+        ps = [_ptr(f, self.cplx, n, "fk") for f in (fk0, fk1, fk2)]
+        pc = _ptr(out, self.real, 3 * self.Np, "c")
+        with torch.cuda.device(self.device):
+            _check(lib().nufft_execute_type2_real3(self._h, *ps, pc), "nufft_execute_type2_real3")
         return out
 
     def spread(self, c: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:

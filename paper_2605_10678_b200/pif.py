@@ -29,7 +29,7 @@ from . import nufft as _n
 class LandauPIF:
     def __init__(self, N, Np, eps=1e-4, dt=0.01, alpha=0.05, k=0.5, precision="f64",
                  comm=None, device=None, seed=1, timing=False, real=None, tile=None,
-                 spread_warps=0):
+                 spread_warps=0, fused=False):
         import synthetic
         self.N = tuple(N)
         self.k, self.alpha, self.dt = k, alpha, dt
@@ -81,7 +81,13 @@ class LandauPIF:
         shape = self.plan.local_shape_real if self.real else self.plan.local_shape
         self.rho_k = torch.empty(shape, dtype=cdt, device=dev)
         self.e_k = [torch.empty(shape, dtype=cdt, device=dev) for _ in range(3)]
-        self.e_pts = torch.empty(self.cap, dtype=rdt if self.real else cdt, device=dev)
+        # per-component field gathers through e_pts; the fused three-field gather +
+        # kick (nufft_pif_gather_kick) is correct but measured slower on B200 (C4:
+        # 808 ms vs 3 x 144 ms: three component tiles halve the resident CTAs of a
+        # shared-memory-latency-bound kernel), so it is opt-in
+        self.fused = fused and self.real and comm is None
+        self.e_pts = (None if self.fused else
+                      torch.empty(self.cap, dtype=rdt if self.real else cdt, device=dev))
         self.t = 0.0
         if comm is not None:
             self.migrate()   # sampling at a slab edge may round into the neighbour's cell
@@ -115,16 +121,22 @@ class LandauPIF:
             _n._check(poisson(p._h, self.rho_k.data_ptr(), *(e.data_ptr() for e in self.e_k)),
                       "nufft_pif_poisson")                                      # (2) field solve
             s = self.qm * self.dt / self.L ** 3
-            e_pts = self.e_pts[:n]
-            kick = L.nufft_pif_kick_real if self.real else L.nufft_pif_kick
-            for e_k, v in zip(self.e_k, (self.vx, self.vy, self.vz)):
-                if self.real:
-                    p.type2_real(e_k, out=e_pts)                                # (3) gather
-                else:
-                    p.type2(e_k, out=e_pts)
-                _n._check(kick(p._h, n, ctypes.c_void_p(v.data_ptr()),
-                               ctypes.c_void_p(e_pts.data_ptr()), ctypes.c_double(s)),
-                          "nufft_pif_kick")                                     # (4) push
+            if self.fused:   # (3) + (4): three-field gather with the kick fused in
+                _n._check(L.nufft_pif_gather_kick(p._h, *(e.data_ptr() for e in self.e_k),
+                                                  *(ctypes.c_void_p(v.data_ptr()) for v in
+                                                    (self.vx, self.vy, self.vz)),
+                                                  ctypes.c_double(s)), "nufft_pif_gather_kick")
+            else:
+                e_pts = self.e_pts[:n]
+                kick = L.nufft_pif_kick_real if self.real else L.nufft_pif_kick
+                for e_k, v in zip(self.e_k, (self.vx, self.vy, self.vz)):
+                    if self.real:
+                        p.type2_real(e_k, out=e_pts)                            # (3) gather
+                    else:
+                        p.type2(e_k, out=e_pts)
+                    _n._check(kick(p._h, n, ctypes.c_void_p(v.data_ptr()),
+                                   ctypes.c_void_p(e_pts.data_ptr()), ctypes.c_double(s)),
+                              "nufft_pif_kick")                                 # (4) push
             _n._check(L.nufft_pif_drift(p._h, n, *(ctypes.c_void_p(a.data_ptr()) for a in
                                                    (self.x, self.y, self.z, self.vx, self.vy, self.vz)),
                                         ctypes.c_double(self.dt)), "nufft_pif_drift")

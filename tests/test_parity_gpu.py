@@ -125,6 +125,27 @@ def test_stage_spread_and_interp_match_oracle(nb):
     assert oracle.rel_l2(gi, oracle.interp(x, y, z, grid, w, beta, TWO_PI)) <= 1e-12
 
 
+def test_stage_calls_never_write_past_the_callers_grid(nb):
+    # nufft_spread writes exactly nf1 nf2 nf3 complex cells (device and host buffers)
+    N, Np, eps = (8, 10, 12), 3000, 1e-6
+    pts, c = host_inputs(Np, "f64", seed=5)
+    plan = nb.Plan(N, eps, precision="f64")
+    plan.setpts(*(dev(p) for p in pts))
+    n = 8 * N[0] * N[1] * N[2]
+    shape = (2 * N[2], 2 * N[1], 2 * N[0])
+    for on_dev in (True, False):
+        guard = torch.full((n + 4096,), 7.0 + 7.0j, dtype=torch.complex128)
+        if on_dev:
+            guard = guard.cuda()
+        else:
+            guard = guard.pin_memory()
+        g = guard[:n].view(shape)
+        plan.spread(dev(c) if on_dev else c, out=g)
+        torch.cuda.synchronize()
+        assert bool((guard[n:] == 7.0 + 7.0j).all())
+        assert float(g.abs().max()) > 0
+
+
 def test_nonuniform_shape_signs_modeord_landau(nb):
     N, Np, eps = (8, 12, 20), 6000, 1e-8
     L = 4 * math.pi

@@ -107,3 +107,35 @@ def test_real_pif_like_hermitian_field_and_edge_cases(nb):
     f0 = plan0.type1_real(e)
     assert float(f0.abs().max()) == 0.0
     assert plan0.type2_real(fh).numel() == 0
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("eps", [1e-4, 1e-7])
+def test_three_field_gather_and_fused_kick(nb, prec, eps):
+    # type2_real3 == three type2_real calls; gather_kick == type2_real + kick per component
+    if prec == "f32" and eps < 1e-6:
+        eps = 1e-6
+    N, Np = (16, 20, 24), 20000
+    pts, _ = inputs(Np, prec, seed=24)
+    cdt = torch.complex128 if prec == "f64" else torch.complex64
+    fks = [synthetic.modes(*N, seed=40 + d).to(cdt).cuda() for d in range(3)]
+    plan = nb.Plan(N, eps, precision=prec)
+    plan.setpts(*(p.cuda() for p in pts))
+    sep = torch.stack([plan.type2_real(f) for f in fks], dim=1)
+    vec = plan.type2_real3(*fks)
+    tol = 1e-13 if prec == "f64" else 1e-5
+    assert float((vec - sep).abs().max() / sep.abs().max()) <= tol
+    # against the oracle too
+    x, y, z = (np64(p) for p in pts)
+    ref = np.stack([oracle.type2(x, y, z, np64(f), eps).real for f in fks], axis=1)
+    assert np.linalg.norm(np64(vec) - ref) / np.linalg.norm(ref) <= TOL[prec]
+    rdt = torch.float64 if prec == "f64" else torch.float32
+    v = [torch.randn(Np, dtype=rdt, device="cuda") for _ in range(3)]
+    v_ref = [a + 0.37 * sep[:, d] for d, a in enumerate(v)]
+    lib = nb.lib()
+    import ctypes
+    rc = lib.nufft_pif_gather_kick(plan._h, *(f.data_ptr() for f in fks),
+                                   *(ctypes.c_void_p(a.data_ptr()) for a in v), ctypes.c_double(0.37))
+    assert rc == 0
+    for a, b in zip(v, v_ref):
+        assert float((a - b).abs().max() / b.abs().max()) <= tol
