@@ -77,7 +77,8 @@ typedef struct {
                         * products (both need T_d = 16 - w); 4 / 8 = smem z-plane owners, that many warps */
     int precompute;    /* ES weights of every point (3 w reals, sorted order) computed once by setpts and
                         * read by every execute / spread / interp instead of re-evaluating phi:
-                        * 0 = auto (when they fit in 1/4 of the device memory), 1 = always, -1 = never */
+                        * 0 = auto (fp64 plans, when the table fits in 1/4 of the device memory),
+                        * 1 = always, -1 = never */
     int reserved[5];
 } nufft_opts;
 

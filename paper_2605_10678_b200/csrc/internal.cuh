@@ -87,11 +87,15 @@ template <typename T>
 cudaError_t launch_spread(const Geom& g, const PtsView<T>& p, int64_t nbins,
                           const typename Cx<T>::type* c, typename Cx<T>::type* grid, double beta,
                           cudaStream_t s);
-// interp.cu: c = C^T grid
+// interp.cu: c = C^T grid.  tmap (optional): a CUtensorMap of `grid` (reals, box =
+// pitch x (T1 + w) x (T2 + w) cells, interp_tile_pitch): interior bins stage their
+// subgrid with one TMA tensor copy
 template <typename T>
 cudaError_t launch_interp(const Geom& g, const PtsView<T>& p, int64_t nbins,
                           const typename Cx<T>::type* grid, typename Cx<T>::type* c, double beta,
-                          cudaStream_t s);
+                          cudaStream_t s, const void* tmap = nullptr);
+// smem row pitch (cells) of the interp's subgrid for complex cells of cell_bytes
+int interp_tile_pitch(int cell_bytes, int T, int W);
 template <typename T>
 cudaError_t launch_spread_real(const Geom& g, const PtsView<T>& p, int64_t nbins, const T* c,
                                T* grid, double beta, cudaStream_t s);

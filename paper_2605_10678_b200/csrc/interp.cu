@@ -22,6 +22,10 @@
 // reads 8 consecutive cells of ONE row (x = lane % 8, y = lane / 8 + 4 pass),
 // conflict-free for any row pitch; for w <= 5 the flat map over the w^2 columns
 // wastes fewer lanes.
+#include <cuda.h>
+
+#include <cstring>
+
 #include "device_util.cuh"
 #include "internal.cuh"
 
@@ -133,7 +137,8 @@ __device__ __forceinline__ T reduce4(const T (&v)[4], int lane) {
 template <typename T, typename V, int W, typename Out>
 __global__ void __launch_bounds__(kInterpThreads, 2)
     interp_tile_kernel(Geom g, PtsView<T> p, const typename Layout<V>::Cell* __restrict__ grid,
-                       int64_t gstride, Out out, T beta) {
+                       int64_t gstride, Out out, T beta, const __grid_constant__ CUtensorMap tmap,
+                       int use_tmap) {
     using C = V;
     using Cell = typename Layout<V>::Cell;
     constexpr int NCOMP = Layout<V>::comps;  // component tiles (3 for the SoA 3-vector)
@@ -143,7 +148,7 @@ __global__ void __launch_bounds__(kInterpThreads, 2)
     constexpr int XS = W <= 8 ? 8 : 16, YS = 32 / XS, NPASS = (W + YS - 1) / YS;
     constexpr int WS = InterpSmem<T, V, W>::WS;
     constexpr int NW = kInterpWarps;
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(1024) unsigned char smem[];  // TMA tensor destination
 
     const int b = blockIdx.x;
     const uint32_t beg = p.offset[b], end = p.offset[b + 1];
@@ -160,13 +165,30 @@ __global__ void __launch_bounds__(kInterpThreads, 2)
         (reinterpret_cast<uintptr_t>(reinterpret_cast<T*>(tile + NCOMP * ncell) + NW * 32 * WS) + 15) &
         ~(uintptr_t)15);
 
-    // ---- stage the subgrid with bulk copies (one mbarrier transaction)
+    // ---- stage the subgrid (one mbarrier transaction).  A bin whose subgrid lies
+    // inside the grid (no periodic wrap) is ONE 3D TMA tensor copy of the whole box;
+    // the others take one bulk copy per row segment, split at the periodic boundary.
+    const int oy0 = by * g.T[1] - W / 2, oz0 = bz * g.T[2] - W / 2;
+    const bool interior = use_tmap && tx.gx0 >= 0 && tx.gx0 + tx.len <= (int)g.nf[0] &&
+                          oy0 >= 0 && oy0 + Ey <= (int)g.nf[1] && oz0 >= 0 &&
+                          oz0 + Ez <= (int)g.nz_loc;
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
-        mbar_arrive_expect_tx(bar, (unsigned)(NCOMP * Ey * Ez * tx.len * sizeof(Cell)));
+        mbar_arrive_expect_tx(bar, interior ? (unsigned)(Ez * Ey * pitch * sizeof(Cell))
+                                            : (unsigned)(NCOMP * Ey * Ez * tx.len * sizeof(Cell)));
     }
     __syncthreads();
-    {
+    if (interior) {
+        if (threadIdx.x == 0) {
+            constexpr int R = (int)(sizeof(Cell) / sizeof(T));  // map elements per cell
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_addr(tile)),
+                "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(tx.gx0 * R), "r"(oy0), "r"(oz0),
+                "r"(smem_addr(bar))
+                : "memory");
+        }
+    } else {
         const int oy = by * g.T[1] - W / 2, oz = bz * g.T[2] - W / 2;
         const int nfx = (int)g.nf[0], nfy = (int)g.nf[1];
         int sg[2], ss[2], sn[2];
@@ -328,7 +350,7 @@ size_t smem_w(const Geom& g) {
 template <typename T, typename V, int W, typename Out = StoreOut<V>>
 cudaError_t launch_w(const Geom& g, const PtsView<T>& p, int64_t nbins,
                      const typename Layout<V>::Cell* grid, Out c, double beta, cudaStream_t s,
-                     int64_t gstride = 0) {
+                     int64_t gstride = 0, const void* tmap = nullptr) {
     const size_t smem = smem_w<T, V, W>(g);
     auto kern = interp_tile_kernel<T, V, W, Out>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -337,8 +359,12 @@ cudaError_t launch_w(const Geom& g, const PtsView<T>& p, int64_t nbins,
         cudaGetLastError();
         return e;
     }
+    CUtensorMap map;
+    std::memset(&map, 0, sizeof(map));
+    if (tmap) std::memcpy(&map, tmap, sizeof(map));
     if (nbins > 0)
-        kern<<<(unsigned)nbins, kInterpThreads, smem, s>>>(g, p, grid, gstride, c, (T)beta);
+        kern<<<(unsigned)nbins, kInterpThreads, smem, s>>>(g, p, grid, gstride, c, (T)beta, map,
+                                                           tmap ? 1 : 0);
     return cudaGetLastError();
 }
 
@@ -357,9 +383,10 @@ cudaError_t launch_w(const Geom& g, const PtsView<T>& p, int64_t nbins,
 template <typename T>
 cudaError_t launch_interp(const Geom& g, const PtsView<T>& p, int64_t nbins,
                           const typename Cx<T>::type* grid, typename Cx<T>::type* c, double beta,
-                          cudaStream_t s) {
-#define CALL(WW) \
-    launch_w<T, typename Cx<T>::type, WW>(g, p, nbins, grid, StoreOut<typename Cx<T>::type>{c}, beta, s)
+                          cudaStream_t s, const void* tmap) {
+#define CALL(WW)                                                                            \
+    launch_w<T, typename Cx<T>::type, WW>(g, p, nbins, grid, StoreOut<typename Cx<T>::type>{c}, \
+                                          beta, s, 0, tmap)
     NUFFT_W_SWITCH(CALL)
 #undef CALL
     return cudaErrorInvalidValue;
@@ -408,10 +435,16 @@ size_t interp_smem_bytes(const Geom& g) {
     return 0;
 }
 
+int interp_tile_pitch(int cell_bytes, int T, int W) {
+    return cell_bytes == 16 ? tile_pitch<16>(T, W) : tile_pitch<8>(T, W);
+}
+
 template cudaError_t launch_interp<float>(const Geom&, const PtsView<float>&, int64_t,
-                                          const float2*, float2*, double, cudaStream_t);
+                                          const float2*, float2*, double, cudaStream_t,
+                                          const void*);
 template cudaError_t launch_interp<double>(const Geom&, const PtsView<double>&, int64_t,
-                                           const double2*, double2*, double, cudaStream_t);
+                                           const double2*, double2*, double, cudaStream_t,
+                                           const void*);
 template cudaError_t launch_interp_real<float>(const Geom&, const PtsView<float>&, int64_t,
                                                const float*, float*, double, cudaStream_t);
 template cudaError_t launch_interp_real<double>(const Geom&, const PtsView<double>&, int64_t,

@@ -7,12 +7,14 @@
 // of the NUFFT itself runs in the kernels of sort.cu / spread*.cu / interp.cu /
 // elementwise.cu (and cuFFT for the uniform FFT).  Plans with
 // opts.comm are z-slab plans whose execute path lives in dist.cpp.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cufft.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -215,7 +217,9 @@ int local_sort(nufft_plan_s* p, int64_t Np, const void* xd, const void* yd, cons
     p->Np = Np;
     // per-point ES weights, reused by every execute on these points
     p->wts_on = false;
-    if (p->precompute >= 0 && Np > 0) {
+    // auto (0): fp64 only -- fp32 weights are cheap to evaluate in the kernels (expf) and
+    // the table did not pay at C2b (1.868 vs 1.883 ms per step); 1 forces it, -1 never
+    if ((p->precompute > 0 || (p->precompute == 0 && p->prec == NUFFT_F64)) && Np > 0) {
         const size_t need = (size_t)Np * 3 * (size_t)p->w * p->real_size;
         bool want = p->precompute > 0 || p->wts_bytes >= need;  // no query when it fits
         if (!want) {  // auto: when the table fits in a quarter of the device memory
@@ -347,16 +351,69 @@ void* half_spectrum(nufft_plan_s* p) {
     return static_cast<char*>(p->d_grid) + (size_t)(p->nf[0] * p->nf[1] * p->nf[2]) * p->real_size;
 }
 
+// The interp's subgrid box as a TMA tensor map over the complex grid at grid0
+// (reals: {2 nf1, nf2, nz_loc}, box {2 pitch, T2 + w, T3 + w}; the box row is the
+// kernel's padded smem row, columns past the grid are zero-filled and unused).
+// Returns the map, or nullptr (the kernel then stages every bin row by row).
+static const void* interp_tmap(nufft_plan_s* p, const void* grid0) {
+    using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Encode encode = nullptr;
+    static int resolved = 0;
+    if (p->tmap_state < 0 || grid0 == nullptr) return nullptr;
+    if (p->tmap_state == 1 && p->tmap_grid == grid0) return p->tmap;
+    if (!resolved) {
+        void* fn = nullptr;
+        if (std::getenv("NUFFT_NO_TMAP")) {  // ablation switch (profiles/README.md)
+            resolved = 1;
+            return nullptr;
+        }
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+                cudaSuccess && q == cudaDriverEntryPointSuccess)
+            encode = reinterpret_cast<Encode>(fn);
+        resolved = 1;
+    }
+    const int w = p->w, r = (int)p->real_size;
+    const int pitch = interp_tile_pitch(2 * r, p->geom.T[0], w);
+    const cuuint64_t dim[3] = {(cuuint64_t)(2 * p->nf[0]), (cuuint64_t)p->nf[1],
+                               (cuuint64_t)p->geom.nz_loc};
+    const cuuint64_t stride[2] = {(cuuint64_t)(2 * p->nf[0] * r),
+                                  (cuuint64_t)(2 * p->nf[0] * p->nf[1] * r)};
+    const cuuint32_t box[3] = {(cuuint32_t)(2 * pitch), (cuuint32_t)(p->geom.T[1] + w),
+                               (cuuint32_t)(p->geom.T[2] + w)};
+    const cuuint32_t estride[3] = {1, 1, 1};
+    if (!encode || box[0] > 256 || box[1] > 256 || box[2] > 256 || (box[0] * r) % 16 ||
+        (stride[0] % 16) || (reinterpret_cast<uintptr_t>(grid0) % 16)) {
+        p->tmap_state = -1;
+        return nullptr;
+    }
+    if (encode(reinterpret_cast<CUtensorMap*>(p->tmap),
+               r == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+               const_cast<void*>(grid0), dim, stride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+        p->tmap_state = -1;
+        return nullptr;
+    }
+    p->tmap_state = 1;
+    p->tmap_grid = grid0;
+    return p->tmap;
+}
+
 int do_interp(nufft_plan_s* p, const void* grid0, void* c_dev) {
     StageTimer tm(p, EV_INTERP);
+    const void* tmap = interp_tmap(p, grid0);
     if (p->prec == NUFFT_F64)
         NUFFT_CK(launch_interp<double>(p->geom, pts_view<double>(p), p->nbins,
                                        static_cast<const double2*>(grid0),
-                                       static_cast<double2*>(c_dev), p->beta, p->stream));
+                                       static_cast<double2*>(c_dev), p->beta, p->stream, tmap));
     else
         NUFFT_CK(launch_interp<float>(p->geom, pts_view<float>(p), p->nbins,
                                       static_cast<const float2*>(grid0),
-                                      static_cast<float2*>(c_dev), p->beta, p->stream));
+                                      static_cast<float2*>(c_dev), p->beta, p->stream, tmap));
     return NUFFT_OK;
 }
 

@@ -52,6 +52,12 @@ struct nufft_plan_s {
     uint32_t* bin_of = nullptr;   // setpts scratch when the grid buffer cannot host it
     uint32_t* rank_of = nullptr;
     size_t scratch_cap = 0;
+    // TMA tensor map of the complex grid the interp last read (CUtensorMap, 128 B,
+    // opaque here): rebuilt when the grid address changes; tmap_state -1 = the driver
+    // entry point is unavailable (the interp keeps its row copies)
+    alignas(64) unsigned char tmap[128] = {};
+    const void* tmap_grid = nullptr;
+    int tmap_state = 0;
     void* rec = nullptr;  // Np sorted 32-byte records (PtRec)
     // per-point ES weights (opts.precompute): Np x 3w reals in sorted order
     int precompute = 0;     // opts value: 0 auto, 1 always, -1 never
