@@ -74,12 +74,19 @@ typedef struct {
     int tile[3];       /* bin edge T_d (fine cells); 0 = built-in table by w; T_d + w + 2 <= 2 N_d  */
     int timing;        /* 1 = record per-stage CUDA events (read back by nufft_get_info)              */
     int spread_warps;  /* spread kernel: 0 = built-in choice; 1 = register rows, 2 = register outer   *
-                        * products (both need T_d = 16 - w); 4 / 8 = smem z-plane owners, that many warps */
+                        * products (both need T_d = 16 - w); 4 / 8 = smem z-plane owners, that many warps; *
+                        * ablation only (complex transforms; real ones use 8): -1 = the paper's Atomic    *
+                        * Spread, one thread per point in caller order, global atomics;*
+                        * -2 = the same over the bin-sorted points                                        */
     int precompute;    /* ES weights of every point (3 w reals, sorted order) computed once by setpts and
                         * read by every execute / spread / interp instead of re-evaluating phi:
                         * 0 = auto (fp64 plans, when the table fits in 1/4 of the device memory),
                         * 1 = always, -1 = never */
-    int reserved[5];
+    int interp_method; /* 0 = tiled (subgrid staged in shared memory, default); ablation only (complex *
+                        * type 2 / nufft_interp): 1 = the paper's Direct Interpolation, one thread per    *
+                        * point in caller order reading global memory; 2 = the same   *
+                        * over the bin-sorted points                                   */
+    int reserved[4];
 } nufft_opts;
 
 typedef struct {

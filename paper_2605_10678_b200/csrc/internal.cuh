@@ -94,6 +94,21 @@ template <typename T>
 cudaError_t launch_interp(const Geom& g, const PtsView<T>& p, int64_t nbins,
                           const typename Cx<T>::type* grid, typename Cx<T>::type* c, double beta,
                           cudaStream_t s, const void* tmap = nullptr);
+// variants.cu (ablation only): the paper's Atomic Spread and
+// Direct Interpolation, one thread per point; order =
+// sorted slot of caller point t (caller-order walk) or nullptr (bin-sorted walk)
+template <typename T>
+cudaError_t launch_spread_atomic(const Geom& g, const PtsView<T>& p, int64_t nbins,
+                                 const uint32_t* order, int64_t Np, const typename Cx<T>::type* c,
+                                 typename Cx<T>::type* grid, double beta, cudaStream_t s);
+template <typename T>
+cudaError_t launch_interp_direct(const Geom& g, const PtsView<T>& p, int64_t nbins,
+                                 const uint32_t* order, int64_t Np,
+                                 const typename Cx<T>::type* grid, typename Cx<T>::type* c,
+                                 double beta, cudaStream_t s);
+template <typename T>
+cudaError_t launch_caller_order(const PtRec<T>* rec, int64_t Np, uint32_t* order,
+                                cudaStream_t s);
 // smem row pitch (cells) of the interp's subgrid for complex cells of cell_bytes
 int interp_tile_pitch(int cell_bytes, int T, int W);
 template <typename T>

@@ -215,6 +215,7 @@ int local_sort(nufft_plan_s* p, int64_t Np, const void* xd, const void* yd, cons
                                         p->blocksum, bin_of, rank_of,
                                         static_cast<PtRec<float>*>(p->rec), p->nbins, p->stream));
     p->Np = Np;
+    p->order_ok = false;
     // per-point ES weights, reused by every execute on these points
     p->wts_on = false;
     // auto (0): fp64 only -- fp32 weights are cheap to evaluate in the kernels (expf) and
@@ -258,8 +259,45 @@ int local_sort(nufft_plan_s* p, int64_t Np, const void* xd, const void* yd, cons
     return NUFFT_OK;
 }
 
+// caller-order walk of the ablation variants: order[t] = sorted slot of caller point t
+static int caller_order(nufft_plan_s* p, const uint32_t** out) {
+    if (!p->order_ok) {
+        if (p->Np > p->order_cap) {
+            dev_free(p, &p->order, 4 * p->order_cap);
+            p->order_cap = 0;
+            int st = dev_alloc(p, &p->order, 4 * (size_t)p->Np);
+            if (st) return st;
+            p->order_cap = p->Np;
+        }
+        NUFFT_CK(p->prec == NUFFT_F64
+                     ? launch_caller_order<double>(static_cast<const PtRec<double>*>(p->rec), p->Np,
+                                                   static_cast<uint32_t*>(p->order), p->stream)
+                     : launch_caller_order<float>(static_cast<const PtRec<float>*>(p->rec), p->Np,
+                                                  static_cast<uint32_t*>(p->order), p->stream));
+        p->order_ok = true;
+    }
+    *out = static_cast<const uint32_t*>(p->order);
+    return NUFFT_OK;
+}
+
 int do_spread(nufft_plan_s* p, const void* c_dev, void* grid0) {
     StageTimer tm(p, EV_SPREAD);
+    if (p->geom.spread_warps < 0) {  // Atomic Spread (-1 caller order, -2 bin-sorted)
+        const uint32_t* order = nullptr;
+        if (p->geom.spread_warps == -1) {
+            int st = caller_order(p, &order);
+            if (st) return st;
+        }
+        if (p->prec == NUFFT_F64)
+            NUFFT_CK(launch_spread_atomic<double>(p->geom, pts_view<double>(p), p->nbins, order,
+                                                  p->Np, static_cast<const double2*>(c_dev),
+                                                  static_cast<double2*>(grid0), p->beta, p->stream));
+        else
+            NUFFT_CK(launch_spread_atomic<float>(p->geom, pts_view<float>(p), p->nbins, order,
+                                                 p->Np, static_cast<const float2*>(c_dev),
+                                                 static_cast<float2*>(grid0), p->beta, p->stream));
+        return NUFFT_OK;
+    }
     const bool rows = p->geom.spread_warps == 1;  // register-row kernel (plan checked it applies)
     const bool outer = p->geom.spread_warps == 2;  // plane outer-product kernel (ditto)
     if (outer && p->prec == NUFFT_F64)
@@ -293,7 +331,8 @@ int do_spread(nufft_plan_s* p, const void* c_dev, void* grid0) {
 int do_spread_real(nufft_plan_s* p, const void* c_dev, void* grid) {
     StageTimer tm(p, EV_SPREAD);
     Geom g = p->geom;
-    if (g.spread_warps == 1) g.spread_warps = 8;  // no real register-row kernel
+    // no real register-row or ablation kernels: real transforms take the z-plane owners
+    if (g.spread_warps == 1 || g.spread_warps < 0) g.spread_warps = 8;
     if (g.spread_warps == 2 && p->prec == NUFFT_F64)
         NUFFT_CK(launch_spread_outer_real<double>(g, pts_view<double>(p), p->nbins,
                                                   static_cast<const double*>(c_dev),
@@ -405,6 +444,22 @@ static const void* interp_tmap(nufft_plan_s* p, const void* grid0) {
 
 int do_interp(nufft_plan_s* p, const void* grid0, void* c_dev) {
     StageTimer tm(p, EV_INTERP);
+    if (p->interp_method > 0) {  // Direct Interpolation (1 caller order, 2 bin-sorted)
+        const uint32_t* order = nullptr;
+        if (p->interp_method == 1) {
+            int st = caller_order(p, &order);
+            if (st) return st;
+        }
+        if (p->prec == NUFFT_F64)
+            NUFFT_CK(launch_interp_direct<double>(p->geom, pts_view<double>(p), p->nbins, order,
+                                                  p->Np, static_cast<const double2*>(grid0),
+                                                  static_cast<double2*>(c_dev), p->beta, p->stream));
+        else
+            NUFFT_CK(launch_interp_direct<float>(p->geom, pts_view<float>(p), p->nbins, order,
+                                                 p->Np, static_cast<const float2*>(grid0),
+                                                 static_cast<float2*>(c_dev), p->beta, p->stream));
+        return NUFFT_OK;
+    }
     const void* tmap = interp_tmap(p, grid0);
     if (p->prec == NUFFT_F64)
         NUFFT_CK(launch_interp<double>(p->geom, pts_view<double>(p), p->nbins,
@@ -506,8 +561,10 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
     else nufft_default_opts(&o);
     if (!(o.L > 0) || (o.modeord != 0 && o.modeord != 1)) return NUFFT_ERR_ARG;
     if (o.spread_warps != 0 && o.spread_warps != 1 && o.spread_warps != 2 &&
-        o.spread_warps != 4 && o.spread_warps != 8)
+        o.spread_warps != 4 && o.spread_warps != 8 && o.spread_warps != -1 &&
+        o.spread_warps != -2)
         return NUFFT_ERR_ARG;
+    if (o.interp_method < 0 || o.interp_method > 2) return NUFFT_ERR_ARG;
 
     nufft_plan_s* p = new (std::nothrow) nufft_plan_s();
     if (!p) return NUFFT_ERR_ALLOC;
@@ -535,6 +592,7 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
         return NUFFT_ERR_ARG;
     }
     p->precompute = o.precompute;
+    p->interp_method = o.interp_method;
 
     Geom& g = p->geom;
     for (int d = 0; d < 3; ++d) {
@@ -972,6 +1030,7 @@ int nufft_destroy(nufft_handle p) {
     dev_free(p, (void**)&p->rank_of, 0);
     dev_free(p, &p->rec, 0);
     dev_free(p, &p->wts, 0);
+    dev_free(p, &p->order, 0);
     dev_free(p, &p->stage_in, 0);
     dev_free(p, &p->stage_out, 0);
     if (p->timing)

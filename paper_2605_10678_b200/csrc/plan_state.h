@@ -59,6 +59,12 @@ struct nufft_plan_s {
     const void* tmap_grid = nullptr;
     int tmap_state = 0;
     void* rec = nullptr;  // Np sorted 32-byte records (PtRec)
+    // ablation variants (variants.cu, opts.spread_warps < 0 / opts.interp_method > 0):
+    // sorted slot of every caller point, built on first use after each setpts
+    int interp_method = 0;
+    void* order = nullptr;
+    int64_t order_cap = 0;
+    bool order_ok = false;
     // per-point ES weights (opts.precompute): Np x 3w reals in sorted order
     int precompute = 0;     // opts value: 0 auto, 1 always, -1 never
     void* wts = nullptr;

@@ -34,7 +34,7 @@ class Opts(ctypes.Structure):
                 ("comm", ctypes.c_void_p), ("points_owned", ctypes.c_int),
                 ("tile", ctypes.c_int * 3), ("timing", ctypes.c_int),
                 ("spread_warps", ctypes.c_int), ("precompute", ctypes.c_int),
-                ("reserved", ctypes.c_int * 5)]
+                ("interp_method", ctypes.c_int), ("reserved", ctypes.c_int * 4)]
 
 
 class Info(ctypes.Structure):
@@ -160,11 +160,15 @@ class Plan:
     comm     : a Comm -> z-slab plan over its ranks (modes are y-slabs: local_modes())
     points_owned : distributed only; 1 = every point given lies in this rank's z-slab
     precompute : ES weights per point stored by setpts (0 auto, 1 always, -1 never)
+    spread_warps : spread kernel (include/nufft.h); -1 / -2 = the paper's Atomic Spread
+                   in caller / bin-sorted order (ablation only)
+    interp_method: 0 tiled (default); 1 / 2 = the paper's Direct Interpolation in
+                   caller / bin-sorted order (ablation only)
     """
 
     def __init__(self, N, eps, precision="f64", iflag=-1, L=2 * math.pi, modeord=0,
                  device=None, stream=None, tile=None, timing=False, spread_warps=0,
-                 comm=None, points_owned=False, precompute=0):
+                 comm=None, points_owned=False, precompute=0, interp_method=0):
         if not torch.cuda.is_available():
             raise NufftError("libnufft requires a CUDA device (no CPU fallback)")
         self.N = tuple(int(n) for n in N)
@@ -183,6 +187,7 @@ class Plan:
         o.timing = 1 if timing else 0
         o.spread_warps = int(spread_warps)
         o.precompute = int(precompute)
+        o.interp_method = int(interp_method)
         if comm is not None:
             o.comm = comm._h
             o.points_owned = 1 if points_owned else 0

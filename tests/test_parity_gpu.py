@@ -200,6 +200,35 @@ def test_precomputed_weights_both_paths(nb, prec, kernel, precompute):
     assert oracle.rel_l2(g2, oracle.type2(x, y, z, np64(fk), eps)) <= TOL[prec]
 
 
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("variant", [(-1, 1), (-2, 2)])
+@pytest.mark.parametrize("precompute", [-1, 1])
+def test_ablation_variants_atomic_spread_direct_interp(nb, prec, variant, precompute):
+    # the paper's Atomic Spread / Direct Interpolation,
+    # in caller order (-1 / 1) and bin-sorted order (-2 / 2), clustered points
+    # included (atomic contention), to the same oracle bars as the default kernels
+    sw, im = variant
+    eps = 1e-9 if prec == "f64" else 1e-5
+    N, Np = (20, 24, 16), 25000
+    x, y, z = synthetic.clustered_points(Np, seed=13)
+    rdt = torch.float64 if prec == "f64" else torch.float32
+    pts = (x.to(rdt), y.to(rdt), z.to(rdt))
+    cdt = torch.complex128 if prec == "f64" else torch.complex64
+    c = synthetic.strengths(Np).to(cdt)
+    fk = synthetic.modes(*N).to(cdt)
+    plan, g1, g2 = run_pair(nb, N, eps, prec, pts, c, fk, spread_warps=sw, interp_method=im,
+                            precompute=precompute)
+    xs, ys, zs = (np64(p) for p in pts)
+    assert oracle.rel_l2(g1, oracle.type1(xs, ys, zs, np64(c), N, eps)) <= TOL[prec]
+    assert oracle.rel_l2(g2, oracle.type2(xs, ys, zs, np64(fk), eps)) <= TOL[prec]
+    # a second setpts (other points, fewer of them) refreshes the caller-order map
+    pts2, c2 = host_inputs(Np // 3, prec, seed=14)
+    plan.setpts(*(p.cuda() for p in pts2))
+    f = np64(plan.type2(fk.cuda()))
+    xs, ys, zs = (np64(p) for p in pts2)
+    assert oracle.rel_l2(f, oracle.type2(xs, ys, zs, np64(fk), eps)) <= TOL[prec]
+
+
 def test_custom_and_ragged_tiles(nb):
     N, Np, eps = (32, 32, 32), 30000, 1e-5
     pts, c = host_inputs(Np, "f64", seed=7)
