@@ -476,12 +476,14 @@ int do_interp(nufft_plan_s* p, const void* grid0, void* c_dev) {
 
 namespace {
 
-// Default bin edge by width (measured on B200, profiles/README.md): the register
-// outer-product spread takes a 16 x 16 x 16 subgrid (T = 16 - w) -- the default
-// for fp32 and for fp64 with w >= 6; fp64 with w <= 5 uses the shared-memory
-// z-plane spread with T = 8; never larger than the grid allows.
+// Default bin edge by width (measured on B200: profiles/tile_sweep_r01.txt, the
+// exhaustive sweep of scripts/tile_sweep.py): the register outer-product spread
+// takes a 16 x 16 x 16 subgrid (T = 16 - w) -- the default for fp32 and for fp64
+// with 6 <= w <= 12; fp64 with w <= 5 and every w >= 13 use the shared-memory
+// z-plane spread with T = 8 (w = 13: 93 vs 122 ms at 1 point per cell, T = 4);
+// never larger than the grid allows.
 int default_tile(int w, int prec, int64_t nf) {
-    int t = (prec == NUFFT_F64 && w <= 5) ? 8 : 16 - w;
+    int t = ((prec == NUFFT_F64 && w <= 5) || w >= 13) ? 8 : 16 - w;
     if (t < 4) t = 4;
     if (t > 64) t = 64;
     if (t > nf - w - 2) t = (int)(nf - w - 2);  // T + w + 2 <= nf: one-step periodic wraps, <= 2 row segments
@@ -637,19 +639,29 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
             return NUFFT_ERR_CUDA;
         }
         const bool rows = g.spread_warps == 1, outer = g.spread_warps == 2;
-        const size_t sp =
-            precision == NUFFT_F64
-                ? (outer  ? spread_outer_smem_bytes<double>(g)
-                   : rows ? spread_rows_smem_bytes<double>(g)
-                          : spread_smem_bytes<double>(g))
-                : (outer  ? spread_outer_smem_bytes<float>(g)
-                   : rows ? spread_rows_smem_bytes<float>(g)
-                          : spread_smem_bytes<float>(g));
-        const size_t need = std::max(sp, precision == NUFFT_F64 ? interp_smem_bytes<double>(g)
-                                                                : interp_smem_bytes<float>(g));
-        if (need > (size_t)smem_max) {
-            delete p;
-            return NUFFT_ERR_ARG;
+        const bool auto_tile = o.tile[0] <= 0 && o.tile[1] <= 0 && o.tile[2] <= 0;
+        for (;;) {
+            const size_t sp =
+                precision == NUFFT_F64
+                    ? (outer  ? spread_outer_smem_bytes<double>(g)
+                       : rows ? spread_rows_smem_bytes<double>(g)
+                              : spread_smem_bytes<double>(g))
+                    : (outer  ? spread_outer_smem_bytes<float>(g)
+                       : rows ? spread_rows_smem_bytes<float>(g)
+                              : spread_smem_bytes<float>(g));
+            const size_t need = std::max(sp, precision == NUFFT_F64 ? interp_smem_bytes<double>(g)
+                                                                    : interp_smem_bytes<float>(g));
+            if (need <= (size_t)smem_max) break;
+            // a built-in tile too large for one CTA (the widest kernels) shrinks to fit;
+            // a caller's tile is refused
+            if (!auto_tile || outer || rows || g.T[0] <= 2) {
+                delete p;
+                return NUFFT_ERR_ARG;
+            }
+            for (int d = 0; d < 3; ++d) {
+                if (g.T[d] > 2) --g.T[d];
+                g.nb[d] = (int)((p->nf[d] + g.T[d] - 1) / g.T[d]);
+            }
         }
     }
     int st = NUFFT_OK;
