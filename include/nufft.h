@@ -74,7 +74,8 @@ typedef struct {
     int tile[3];       /* bin edge T_d (fine cells); 0 = built-in table by w; T_d + w + 2 <= 2 N_d  */
     int timing;        /* 1 = record per-stage CUDA events (read back by nufft_get_info)              */
     int spread_warps;  /* spread kernel: 0 = built-in choice; 1 = register rows, 2 = register outer   *
-                        * products (both need T_d = 16 - w); 4 / 8 = smem z-plane owners, that many warps; *
+                        * products, 3 = tcgen05 tensor-core GEMM (3xTF32, fp32 complex only; all three   *
+                        * need T_d = 16 - w); 4 / 8 = smem z-plane owners, that many warps;               *
                         * ablation only (complex transforms; real ones use 8): -1 = the paper's Atomic    *
                         * Spread, one thread per point in caller order, global atomics;*
                         * -2 = the same over the bin-sorted points                                        */

@@ -389,7 +389,7 @@ int dist_init(nufft_plan_s* p) {
     if (g.T[2] > d->nzl) {
         g.T[2] = (int)d->nzl;
         // rows / outer products need T = 16 - w on every axis
-        if (g.spread_warps == 1 || g.spread_warps == 2) g.spread_warps = 8;
+        if (g.spread_warps >= 1 && g.spread_warps <= 3) g.spread_warps = 8;
     }
     g.nb[2] = (int)((d->nzl + g.T[2] - 1) / g.T[2]);
     p->nbins = (int64_t)g.nb[0] * g.nb[1] * g.nb[2];

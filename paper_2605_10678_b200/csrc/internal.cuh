@@ -94,6 +94,10 @@ template <typename T>
 cudaError_t launch_interp(const Geom& g, const PtsView<T>& p, int64_t nbins,
                           const typename Cx<T>::type* grid, typename Cx<T>::type* c, double beta,
                           cudaStream_t s, const void* tmap = nullptr);
+// spread_tc.cu: fp32 complex spread as a tcgen05 3xTF32 GEMM per bin (T = 16 - w)
+bool spread_tc_applies(const Geom& g);
+cudaError_t launch_spread_tc(const Geom& g, const PtsView<float>& p, int64_t nbins,
+                             const float2* c, float2* grid, double beta, cudaStream_t s);
 // variants.cu (ablation only): the paper's Atomic Spread and
 // Direct Interpolation, one thread per point; order =
 // sorted slot of caller point t (caller-order walk) or nullptr (bin-sorted walk)

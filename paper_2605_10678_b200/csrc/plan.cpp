@@ -298,6 +298,12 @@ int do_spread(nufft_plan_s* p, const void* c_dev, void* grid0) {
                                                  static_cast<float2*>(grid0), p->beta, p->stream));
         return NUFFT_OK;
     }
+    if (p->geom.spread_warps == 3) {  // tensor-core GEMM spread (plan checked: fp32, T = 16 - w)
+        NUFFT_CK(launch_spread_tc(p->geom, pts_view<float>(p), p->nbins,
+                                  static_cast<const float2*>(c_dev), static_cast<float2*>(grid0),
+                                  p->beta, p->stream));
+        return NUFFT_OK;
+    }
     const bool rows = p->geom.spread_warps == 1;  // register-row kernel (plan checked it applies)
     const bool outer = p->geom.spread_warps == 2;  // plane outer-product kernel (ditto)
     if (outer && p->prec == NUFFT_F64)
@@ -333,6 +339,7 @@ int do_spread_real(nufft_plan_s* p, const void* c_dev, void* grid) {
     Geom g = p->geom;
     // no real register-row or ablation kernels: real transforms take the z-plane owners
     if (g.spread_warps == 1 || g.spread_warps < 0) g.spread_warps = 8;
+    if (g.spread_warps == 3) g.spread_warps = 2;  // the register outer products
     if (g.spread_warps == 2 && p->prec == NUFFT_F64)
         NUFFT_CK(launch_spread_outer_real<double>(g, pts_view<double>(p), p->nbins,
                                                   static_cast<const double*>(c_dev),
@@ -563,7 +570,7 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
     else nufft_default_opts(&o);
     if (!(o.L > 0) || (o.modeord != 0 && o.modeord != 1)) return NUFFT_ERR_ARG;
     if (o.spread_warps != 0 && o.spread_warps != 1 && o.spread_warps != 2 &&
-        o.spread_warps != 4 && o.spread_warps != 8 && o.spread_warps != -1 &&
+        o.spread_warps != 3 && o.spread_warps != 4 && o.spread_warps != 8 && o.spread_warps != -1 &&
         o.spread_warps != -2)
         return NUFFT_ERR_ARG;
     if (o.interp_method < 0 || o.interp_method > 2) return NUFFT_ERR_ARG;
@@ -622,7 +629,8 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
     g.spread_warps = o.spread_warps;
     if (g.spread_warps == 0) g.spread_warps = spread_outer_applies(g) ? 2 : 8;
     if ((g.spread_warps == 1 && !spread_rows_applies(g)) ||
-        (g.spread_warps == 2 && !spread_outer_applies(g))) {
+        (g.spread_warps == 2 && !spread_outer_applies(g)) ||
+        (g.spread_warps == 3 && (precision != NUFFT_F32 || !spread_tc_applies(g)))) {
         delete p;
         return NUFFT_ERR_UNSUPPORTED;
     }
@@ -638,7 +646,7 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
             delete p;
             return NUFFT_ERR_CUDA;
         }
-        const bool rows = g.spread_warps == 1, outer = g.spread_warps == 2;
+        const bool rows = g.spread_warps == 1, outer = g.spread_warps == 2 || g.spread_warps == 3;
         const bool auto_tile = o.tile[0] <= 0 && o.tile[1] <= 0 && o.tile[2] <= 0;
         for (;;) {
             const size_t sp =

@@ -160,7 +160,8 @@ class Plan:
     comm     : a Comm -> z-slab plan over its ranks (modes are y-slabs: local_modes())
     points_owned : distributed only; 1 = every point given lies in this rank's z-slab
     precompute : ES weights per point stored by setpts (0 auto, 1 always, -1 never)
-    spread_warps : spread kernel (include/nufft.h); -1 / -2 = the paper's Atomic Spread
+    spread_warps : spread kernel (include/nufft.h); 3 = tcgen05 tensor-core GEMM (fp32);
+                   -1 / -2 = the paper's Atomic Spread
                    in caller / bin-sorted order (ablation only)
     interp_method: 0 tiled (default); 1 / 2 = the paper's Direct Interpolation in
                    caller / bin-sorted order (ablation only)

@@ -14,4 +14,5 @@ for cfg in ${CONFIGS:-c2b c3}; do
       -k regex:"${KREGEX:-spread_outer|interp_tile|spread_tile|bin_count|scatter}" -s ${SKIP:-5} -c ${COUNT:-4} \
       -o gpurun_out/prof_${cfg}_${TAG:-r01b} python bench.py $A > gpurun_out/ncu_full_$cfg.log 2>&1
   echo "$cfg full rc=$?"
+  [ -n "$EXPORT" ] && bash scripts/ncu_export.sh gpurun_out/prof_${cfg}_${TAG:-r01b}.ncu-rep
 done

@@ -163,15 +163,17 @@ def test_nonuniform_shape_signs_modeord_landau(nb):
 
 
 @pytest.mark.parametrize("prec", ["f64", "f32"])
-@pytest.mark.parametrize("kernel", [1, 2, 4, 8])
+@pytest.mark.parametrize("kernel", [1, 2, 3, 4, 8])
 @pytest.mark.parametrize("eps", [1e-3, 1e-6, 1e-9])
 def test_every_spread_kernel(nb, prec, kernel, eps):
-    # 1 = register-row spread, 2 = plane outer products (both T = 16 - w),
-    # 4 / 8 = shared-memory z-plane owners
+    # 1 = register-row spread, 2 = plane outer products, 3 = tcgen05 3xTF32 GEMM
+    # (fp32 only; all three T = 16 - w), 4 / 8 = shared-memory z-plane owners
     if prec == "f32" and eps < 1e-7:
         eps = 1e-7
+    if kernel == 3 and prec == "f64":
+        pytest.skip("tensor-core spread is fp32-only")
     w = nb.Plan((8, 8, 8), eps, precision=prec).info()["w"]
-    tile = 16 - w if kernel in (1, 2) else 8
+    tile = 16 - w if kernel in (1, 2, 3) else 8
     N, Np = (24, 24, 24), 20000
     pts, c = host_inputs(Np, prec, seed=11)
     fk = synthetic.modes(*N).to(c.dtype)
