@@ -186,14 +186,29 @@ __device__ __forceinline__ TileX tile_x(int bx, int T, int W) {
 }
 
 // ---- grid / strength value types: complex (Eq. 1-2) or real
-__device__ __forceinline__ float2 vscale(float2 a, float s) { return float2{a.x * s, a.y * s}; }
+// complex x real in fp32 uses the packed 2-wide FP32 pipe of sm_100 (SASS FFMA2 /
+// FMUL2, PTX fma.rn.f32x2 / mul.rn.f32x2): one instruction per complex update
+__device__ __forceinline__ uint64_t f2_bits(float2 v) {
+    return (uint64_t)__float_as_uint(v.x) | ((uint64_t)__float_as_uint(v.y) << 32);
+}
+__device__ __forceinline__ float2 f2_from(uint64_t b) {
+    return float2{__uint_as_float((uint32_t)b), __uint_as_float((uint32_t)(b >> 32))};
+}
+__device__ __forceinline__ float2 vscale(float2 a, float s) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(float2{s, s})));
+    return f2_from(r);
+}
 __device__ __forceinline__ double2 vscale(double2 a, double s) { return double2{a.x * s, a.y * s}; }
 __device__ __forceinline__ float vscale(float a, float s) { return a * s; }
 __device__ __forceinline__ double vscale(double a, double s) { return a * s; }
 // acc += z * w
 __device__ __forceinline__ void vfma(float2& acc, float2 z, float w) {
-    acc.x = fmaf(z.x, w, acc.x);
-    acc.y = fmaf(z.y, w, acc.y);
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(r)
+        : "l"(f2_bits(z)), "l"(f2_bits(float2{w, w})), "l"(f2_bits(acc)));
+    acc = f2_from(r);
 }
 __device__ __forceinline__ void vfma(double2& acc, double2 z, double w) {
     acc.x = fma(z.x, w, acc.x);

@@ -25,6 +25,7 @@
 #include <cuda.h>
 
 #include <cstring>
+#include <type_traits>
 
 #include "device_util.cuh"
 #include "internal.cuh"
@@ -95,6 +96,29 @@ template <typename T> struct Layout<Vec3<T>> {
         return Vec3<T>{{t[o], t[o + nc], t[o + 2 * nc]}};
     }
 };
+
+// sv[m] = sum_k G[col + k plane].m wz[k] over the w planes of one stencil column;
+// complex fp32 cells take one packed FFMA2 per cell (device_util.cuh vfma)
+template <typename V, int W, typename T, int NC>
+__device__ __forceinline__ void zsum(T (&sv)[NC], const typename Layout<V>::Cell* tile, int col,
+                                     int plane, int ncell, const T (&wz)[W]) {
+    if constexpr (std::is_same<V, float2>::value) {
+        float2 a = float2{0.0f, 0.0f};
+#pragma unroll
+        for (int k = 0; k < W; ++k) vfma(a, tile[col + k * plane], wz[k]);
+        sv[0] = a.x;
+        sv[1] = a.y;
+    } else {
+#pragma unroll
+        for (int m = 0; m < NC; ++m) sv[m] = 0;
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+            const V v = Layout<V>::load(tile, col + k * plane, ncell);
+#pragma unroll
+            for (int m = 0; m < NC; ++m) sv[m] += VT<V>::get(v, m) * wz[k];
+        }
+    }
+}
 
 // Output stage of the gather: store the value at the caller's index ...
 template <typename V> struct StoreOut {
@@ -286,14 +310,7 @@ __global__ void __launch_bounds__(kInterpThreads, 2)
                             if (qok[q]) {
                                 const int col = base + qoff[q];
                                 T sv[NC];
-#pragma unroll
-                                for (int m = 0; m < NC; ++m) sv[m] = 0;
-#pragma unroll
-                                for (int k = 0; k < W; ++k) {
-                                    const C v = Layout<V>::load(tile, col + k * plane, ncell);
-#pragma unroll
-                                    for (int m = 0; m < NC; ++m) sv[m] += VT<C>::get(v, m) * wz[k];
-                                }
+                                zsum<C, W>(sv, tile, col, plane, ncell, wz);
                                 const T wxy = wj[qx[q]] * wj[W + qy[q]];
 #pragma unroll
                                 for (int m = 0; m < NC; ++m) acc[m][g4] += sv[m] * wxy;
@@ -307,14 +324,7 @@ __global__ void __launch_bounds__(kInterpThreads, 2)
                             if (sx < W && y < W) {
                                 const int col = col0 + y * pitch;
                                 T sv[NC];
-#pragma unroll
-                                for (int m = 0; m < NC; ++m) sv[m] = 0;
-#pragma unroll
-                                for (int k = 0; k < W; ++k) {
-                                    const C v = Layout<V>::load(tile, col + k * plane, ncell);
-#pragma unroll
-                                    for (int m = 0; m < NC; ++m) sv[m] += VT<C>::get(v, m) * wz[k];
-                                }
+                                zsum<C, W>(sv, tile, col, plane, ncell, wz);
                                 const T wy = wj[W + y];
 #pragma unroll
                                 for (int m = 0; m < NC; ++m) acc[m][g4] += sv[m] * wy;
