@@ -240,7 +240,8 @@ def run_ours(args, cfg):
     comm = nb.Comm() if ws > 1 else None   # z-slab plan over NCCL
     plan = nb.Plan(N, cfg["eps"], precision=cfg["prec"], timing=True, device=device,
                    tile=args.tile, spread_warps=args.spread_warps, comm=comm,
-                   points_owned=ws > 1, interp_method=args.interp_method)
+                   points_owned=ws > 1, interp_method=args.interp_method,
+                   precompute=args.precompute)
     pts, c, fk = make_inputs(cfg, rank, ws, device, plan.local_modes() if ws > 1 else None)
     Np = pts[0].numel()
     if args.real:  # real strengths / outputs: the R2C / C2R path
@@ -350,7 +351,8 @@ def run_ours(args, cfg):
                        "w": plan.info()["w"], "precision": cfg["prec"], "points": cfg["kind"],
                        "tile": plan.info()["tile"],
                        "kernels": {"spread_warps": args.spread_warps,
-                                   "interp_method": args.interp_method},
+                                   "interp_method": args.interp_method,
+                                   "weights_precomputed": plan.info()["weights_precomputed"]},
                        "values": "real (R2C / C2R)" if args.real else "complex",
                        "parallelism": (f"z-slab x{ws} (points owned by slab, NCCL halos + "
                                        f"all-to-all)") if ws > 1 else "1 GPU",
@@ -587,6 +589,8 @@ def main():
     ap.add_argument("--tile", default=None, help="bin edge T or Tx,Ty,Tz (default: built-in table)")
     ap.add_argument("--spread-warps", type=int, default=0,
                     help="spread kernel: 1 rows, 2 outer products, 4 / 8 smem planes (default: built-in)")
+    ap.add_argument("--precompute", type=int, default=0,
+                    help="per-point ES weight table: 0 auto (fp64), 1 always, -1 never")
     ap.add_argument("--interp-method", type=int, default=0,
                     help="ablation: 1 / 2 = the paper's Direct Interpolation, caller / sorted order")
     ap.add_argument("--real", action="store_true",

@@ -81,7 +81,7 @@ typedef struct {
                         * -2 = the same over the bin-sorted points                                        */
     int precompute;    /* ES weights of every point (3 w reals, sorted order) computed once by setpts and
                         * read by every execute / spread / interp instead of re-evaluating phi:
-                        * 0 = auto (fp64 plans, when the table fits in 1/4 of the device memory),
+                        * 0 = auto (widths w >= 6, when the table fits in 1/4 of the device memory),
                         * 1 = always, -1 = never */
     int interp_method; /* 0 = tiled (subgrid staged in shared memory, default); ablation only (complex *
                         * type 2 / nufft_interp): 1 = the paper's Direct Interpolation, one thread per    *

@@ -218,9 +218,10 @@ int local_sort(nufft_plan_s* p, int64_t Np, const void* xd, const void* yd, cons
     p->order_ok = false;
     // per-point ES weights, reused by every execute on these points
     p->wts_on = false;
-    // auto (0): fp64 only -- fp32 weights are cheap to evaluate in the kernels (expf) and
-    // the table did not pay at C2b (1.868 vs 1.883 ms per step); 1 forces it, -1 never
-    if ((p->precompute > 0 || (p->precompute == 0 && p->prec == NUFFT_F64)) && Np > 0) {
+    // auto (0): widths w >= 6 (B200, scripts/gpu_precompute.sh, step ms table / in-kernel
+    // phi: C2b fp32 w=7 1.723 / 1.749, C3 fp64 w=7 124.3 / 132.3; at w = 5 the table
+    // does not pay: C2a fp32 1.314 / 1.286, C3e4 fp64 89.3 / 88.8); 1 forces it, -1 never
+    if ((p->precompute > 0 || (p->precompute == 0 && p->w >= 6)) && Np > 0) {
         const size_t need = (size_t)Np * 3 * (size_t)p->w * p->real_size;
         bool want = p->precompute > 0 || p->wts_bytes >= need;  // no query when it fits
         if (!want) {  // auto: when the table fits in a quarter of the device memory
