@@ -35,6 +35,14 @@ __device__ __forceinline__ int64_t index_of(int64_t n, int64_t N, int modeord) {
     return modeord == 0 ? n + N / 2 : (n >= 0 ? n : n + N);
 }
 
+// Row-blocked launch of the pad pass: a block walks fine-grid rows (fixed y, z) with
+// L = 32..256 threads per row and kEwThreads / L rows at a time, so the per-row index
+// arithmetic (64-bit divisions) is done once per row, not once per cell, and rows
+// outside the retained set are a plain zero stream (C2b 74 -> 64 us, C3 529 -> 414 us)
+__host__ __device__ __forceinline__ int row_lanes(int64_t n1) {
+    return n1 <= 32 ? 32 : n1 <= 64 ? 64 : n1 <= 128 ? 128 : 256;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kEwThreads)
     truncate_deconv_kernel(const typename Cx<T>::type* __restrict__ grid, int64_t nf1,
@@ -62,25 +70,31 @@ __global__ void __launch_bounds__(kEwThreads)
                           const T* __restrict__ p3, int modeord, int64_t nf1, int64_t nf2,
                           int64_t nf3, typename Cx<T>::type* __restrict__ grid) {
     using C = typename Cx<T>::type;
-    const int64_t total = nf1 * nf2 * nf3;
-    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < total;
-         m += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t m1 = m % nf1, m2 = (m / nf1) % nf2, m3 = m / (nf1 * nf2);
+    const int L = row_lanes(nf1), RB = kEwThreads / L;
+    const int tx = threadIdx.x % L, ty = threadIdx.x / L;
+    const int64_t rows = nf2 * nf3;
+    for (int64_t r = (int64_t)blockIdx.x * RB + ty; r < rows; r += (int64_t)gridDim.x * RB) {
+        const int64_t m2 = r % nf2, m3 = r / nf2;
+        C* grow = grid + nf1 * r;
         // retained iff m < N/2 (n = m) or m >= nf - N/2 (n = m - nf)
-        const bool k1 = m1 < N1 / 2 || m1 >= nf1 - N1 / 2;
-        const bool k2 = m2 < N2 / 2 || m2 >= nf2 - N2 / 2;
-        const bool k3 = m3 < N3 / 2 || m3 >= nf3 - N3 / 2;
-        C v{0, 0};
-        if (k1 && k2 && k3) {
-            const int64_t n1 = m1 < N1 / 2 ? m1 : m1 - nf1;
-            const int64_t n2 = m2 < N2 / 2 ? m2 : m2 - nf2;
-            const int64_t n3 = m3 < N3 / 2 ? m3 : m3 - nf3;
-            const T s = p1[n1 + N1 / 2] * p2[n2 + N2 / 2] * p3[n3 + N3 / 2];
-            const int64_t i = index_of(n1, N1, modeord) +
-                              N1 * (index_of(n2, N2, modeord) + N2 * index_of(n3, N3, modeord));
-            v = cmul_real(fk[i], s);
+        const bool k23 = (m2 < N2 / 2 || m2 >= nf2 - N2 / 2) && (m3 < N3 / 2 || m3 >= nf3 - N3 / 2);
+        if (!k23) {
+            for (int64_t m1 = tx; m1 < nf1; m1 += L) grow[m1] = C{0, 0};
+            continue;
         }
-        grid[m] = v;
+        const int64_t n2 = m2 < N2 / 2 ? m2 : m2 - nf2;
+        const int64_t n3 = m3 < N3 / 2 ? m3 : m3 - nf3;
+        const T s23 = p2[n2 + N2 / 2] * p3[n3 + N3 / 2];
+        const C* frow =
+            fk + N1 * (index_of(n2, N2, modeord) + N2 * index_of(n3, N3, modeord));
+        for (int64_t m1 = tx; m1 < nf1; m1 += L) {
+            C v{0, 0};
+            if (m1 < N1 / 2 || m1 >= nf1 - N1 / 2) {
+                const int64_t n1 = m1 < N1 / 2 ? m1 : m1 - nf1;
+                v = cmul_real(frow[index_of(n1, N1, modeord)], p1[n1 + N1 / 2] * s23);
+            }
+            grow[m1] = v;
+        }
     }
 }
 
@@ -173,7 +187,7 @@ cudaError_t launch_pad_precorrect(const typename Cx<T>::type* fk, const int64_t 
                                   const T* p1, const T* p2, const T* p3, int modeord,
                                   const int64_t nf[3], typename Cx<T>::type* grid,
                                   cudaStream_t s) {
-    pad_precorrect_kernel<T><<<ew_grid(nf[0] * nf[1] * nf[2]), kEwThreads, 0, s>>>(
+    pad_precorrect_kernel<T><<<ew_grid(nf[1] * nf[2] * row_lanes(nf[0])), kEwThreads, 0, s>>>(
         fk, N[0], N[1], N[2], p1, p2, p3, modeord, nf[0], nf[1], nf[2], grid);
     return cudaGetLastError();
 }
