@@ -125,6 +125,32 @@ def test_stage_spread_and_interp_match_oracle(nb):
     assert oracle.rel_l2(gi, oracle.interp(x, y, z, grid, w, beta, TWO_PI)) <= 1e-12
 
 
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_interp_tensor_map_follows_the_grid_address(nb, prec):
+    # interior bins stage their subgrid through a TMA tensor map of the grid the
+    # interp reads; alternating the plan's own grid (type 2) with two caller grids
+    # (nufft_interp) must re-encode it every time the address changes
+    N, Np, eps = (24, 20, 28), 20000, 1e-6
+    pts, c = host_inputs(Np, prec, seed=8)
+    cdt = torch.complex128 if prec == "f64" else torch.complex64
+    plan = nb.Plan(N, eps, precision=prec)
+    plan.setpts(*(dev(p) for p in pts))
+    info = plan.info()
+    w, beta = info["w"], info["beta"]
+    x, y, z = (np64(p) for p in pts)
+    fk = synthetic.modes(*N).to(cdt)
+    o2 = oracle.type2(x, y, z, np64(fk), eps)
+    rng = np.random.default_rng(9)
+    shape = (2 * N[2], 2 * N[1], 2 * N[0])
+    grids = [rng.standard_normal(shape) + 1j * rng.standard_normal(shape) for _ in range(2)]
+    refs = [oracle.interp(x, y, z, g, w, beta, TWO_PI) for g in grids]
+    dgrids = [dev(torch.from_numpy(g).to(cdt)) for g in grids]
+    for _ in range(2):
+        assert oracle.rel_l2(np64(plan.type2(dev(fk))), o2) <= TOL[prec]
+        for dg, ref in zip(dgrids, refs):
+            assert oracle.rel_l2(np64(plan.interp(dg)), ref) <= (1e-12 if prec == "f64" else 1e-5)
+
+
 def test_stage_calls_never_write_past_the_callers_grid(nb):
     # nufft_spread writes exactly nf1 nf2 nf3 complex cells (device and host buffers)
     N, Np, eps = (8, 10, 12), 3000, 1e-6
