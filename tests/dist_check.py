@@ -31,7 +31,7 @@ def gather_cat(t, dim=0):
     return torch.cat(parts, dim=dim)
 
 
-def run_case(comm, N, Np, eps, prec, owned, kind, L):
+def run_case(comm, N, Np, eps, prec, owned, kind, L, **kw):
     rank, P = dist.get_rank(), dist.get_world_size()
     dev = torch.device("cuda", torch.cuda.current_device())
     rdt = torch.float64 if prec == "f64" else torch.float32
@@ -60,7 +60,7 @@ def run_case(comm, N, Np, eps, prec, owned, kind, L):
             torch.cuda.synchronize()
             print(f"[rank {rank}] {s}", file=sys.stderr, flush=True)
     mark("plan")
-    plan = nb.Plan(N, eps, precision=prec, L=L, comm=comm, points_owned=owned)
+    plan = nb.Plan(N, eps, precision=prec, L=L, comm=comm, points_owned=owned, **kw)
     lo, hi = plan.local_modes()
     mark(f"setpts lo={lo} hi={hi}")
     plan.setpts(xl, yl, zl)
@@ -98,7 +98,7 @@ def run_case(comm, N, Np, eps, prec, owned, kind, L):
         o1 = oracle.rel_l2(f_all.numpy(), oracle.type1(x, y, z, c.numpy().astype(np.complex128), N, eps, L=L))
         o2 = oracle.rel_l2(c2_all.numpy(), oracle.type2(x, y, z, fk.numpy().astype(np.complex128), eps, L=L))
         ok = ok and o1 <= tol_orc and o2 <= tol_orc
-        print(f"P={P} N={N} Np={Np} eps={eps:g} {prec} owned={owned} {kind}: "
+        print(f"P={P} N={N} Np={Np} eps={eps:g} {prec} owned={owned} {kind} {kw}: "
               f"vs 1-GPU {e1:.2e}/{e2:.2e}  vs oracle {o1:.2e}/{o2:.2e}  {'OK' if ok else 'FAIL'}",
               flush=True)
     plan.close()
@@ -186,6 +186,17 @@ def main():
         ((64, 64, 64), 300000, 1e-5, "f64", False, "uniform", 2 * math.pi),
     ]
     ok = all([run_case(comm, *cs) for cs in cases])
+    # kernel options on slabs: the paper's Atomic Spread / Direct Interpolation
+    # (caller and bin-sorted order) and the tcgen05 spread (fp32)
+    opt_cases = [
+        (((32, 32, 32), 40000, 1e-6, "f64", False, "uniform", 2 * math.pi),
+         dict(spread_warps=-1, interp_method=1)),
+        (((32, 32, 32), 40000, 1e-6, "f64", True, "landau", 4 * math.pi),
+         dict(spread_warps=-2, interp_method=2)),
+        (((64, 64, 64), 200000, 1e-5, "f32", True, "uniform", 2 * math.pi),
+         dict(spread_warps=3)),
+    ]
+    ok = all([run_case(comm, *cs, **kw) for cs, kw in opt_cases]) and ok
     real_cases = [
         ((32, 32, 32), 40000, 1e-9, "f64", True, 2 * math.pi),
         ((16, 24, 32), 30000, 1e-6, "f64", False, 4 * math.pi),
