@@ -6,9 +6,8 @@
 // warp-level prefix scans".
 //
 //   k1 bin_count : per point, fold onto the torus and rescale in fp64
-//                  (s = x * nf / L), bin = tile of floor(s); a warp-aggregated
-//                  atomicAdd on count[bin] (lanes of one bin share one atomic via
-//                  __match_any_sync) returns each point's rank inside its bin.
+//                  (s = x * nf / L), bin = tile of floor(s); an atomicAdd on
+//                  count[bin] returns each point's rank inside its bin.
 //   k2 scan      : exclusive prefix sum of count[] -> offset[] with warp
 //                  __shfl_up_sync scans, three phases (tile sums, scan of sums,
 //                  tile scans + carry-in).
@@ -66,17 +65,13 @@ __global__ void __launch_bounds__(kSortThreads) bin_count_kernel(
             bin = (uint32_t)(cx / g.T[0]) +
                   (uint32_t)g.nb[0] * ((uint32_t)(cy / g.T[1]) + (uint32_t)g.nb[1] * (uint32_t)(cz / g.T[2]));
         }
-        // warp-aggregated atomic: one atomicAdd per distinct bin in the warp
-        const unsigned active = __ballot_sync(0xffffffffu, live);
+        // one atomicAdd per point: the rank of the point in its bin.  (A warp-
+        // aggregated __match_any_sync version was measured slower on B200 for the
+        // paper's near-uniform workloads: setpts C2b 0.170 -> 0.152 ms, C3 18.0 ->
+        // 16.5 ms without it; collisions inside a warp are rare at ~1e4-1e5 bins.)
         if (live) {
-            const unsigned peers = __match_any_sync(active, bin);
-            const int leader = __ffs(peers) - 1;
-            const unsigned below = peers & ((1u << lane) - 1u);
-            uint32_t base = 0;
-            if (lane == leader) base = atomicAdd(&count[bin], (uint32_t)__popc(peers));
-            base = __shfl_sync(peers, base, leader);
             bin_of[i] = bin;
-            rank_of[i] = base + (uint32_t)__popc(below);
+            rank_of[i] = atomicAdd(&count[bin], 1u);
         }
     }
 }
