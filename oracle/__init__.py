@@ -29,7 +29,7 @@ _c_int64_p = ctypes.POINTER(ctypes.c_int64)
 def build(force: bool = False) -> str:
     """Compile liboracle.so with g++ (no fast-math, no FMA contraction)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        cmd = ["g++", "-O2", "-std=c++17", "-fopenmp", "-ffp-contract=off", "-fno-fast-math",
+        cmd = ["g++", "-O2", "-std=c++17", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-fcx-limited-range",
                "-shared", "-fPIC", _SRC, "-o", _LIB + ".tmp"]
         subprocess.check_call(cmd)
         os.replace(_LIB + ".tmp", _LIB)
@@ -74,6 +74,9 @@ def lib():
                     ctypes.c_double, ctypes.c_int64, _c_int64_p, _c_double_p]
         L.orc_nudft1.argtypes = nu
         L.orc_nudft2.argtypes = nu
+        L.orc_nudft2_separable.argtypes = pts + [_c_double_p] * 3 + \
+            [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_double,
+             ctypes.c_int64, _c_int64_p, _c_double_p]
         L.orc_num_threads.restype = ctypes.c_int
         L.orc_set_num_threads.argtypes = [ctypes.c_int]
         _lib = L
@@ -229,6 +232,33 @@ def nudft2(x, y, z, fk, iflag=-1, L=2 * np.pi, sel=None):
                          int(iflag), float(L), len(s), s.ctypes.data_as(_c_int64_p),
                          _d(out.view(np.float64)))
     return out
+
+
+def nudft2_separable(x, y, z, a1, a2, a3, iflag=-1, L=2 * np.pi, sel=None):
+    """Exact Eq. (2) for the rank-one mode array fk[n3, n2, n1] = a1[n1] a2[n2] a3[n3]
+    (the triple sum factored into three 1D sums). a_d centered; sel: optional point indices."""
+    x, y, z = _f64(x), _f64(y), _f64(z)
+    a1, a2, a3 = _c128(a1), _c128(a2), _c128(a3)
+    if sel is None:
+        s, ns, sp = None, 0, None
+        out = np.empty(len(x), dtype=np.complex128)
+    else:
+        s = np.ascontiguousarray(sel, dtype=np.int64)
+        ns, sp = len(s), s.ctypes.data_as(_c_int64_p)
+        out = np.empty(len(s), dtype=np.complex128)
+    lib().orc_nudft2_separable(len(x), _d(x), _d(y), _d(z), _d(a1.view(np.float64)),
+                               _d(a2.view(np.float64)), _d(a3.view(np.float64)), len(a1),
+                               len(a2), len(a3), int(iflag), float(L), ns, sp,
+                               _d(out.view(np.float64)))
+    return out
+
+
+def max_abs(a, b) -> float:
+    """max_j |a_j - b_j| / max_j |b_j| (element-wise companion of rel_l2)."""
+    a = np.asarray(a).ravel()
+    b = np.asarray(b).ravel()
+    nb = np.abs(b).max() if b.size else 0.0
+    return float(np.abs(a - b).max() / (nb if nb > 0 else 1.0)) if a.size else 0.0
 
 
 def rel_l2(a, b) -> float:

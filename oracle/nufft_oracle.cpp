@@ -26,7 +26,12 @@
  *
  * Parallelism (OpenMP) never changes results: spreading is partitioned by
  * OUTPUT z-plane (each thread owns disjoint planes and visits points in index
- * order), every other loop is over independent outputs.
+ * order), every other loop is over independent outputs.  Wrapped node indices
+ * are computed once per point (not per cell); the sums are unchanged.  The
+ * sampled NUDFT evaluates only the per-axis phases its modes use.
+ * Build: g++ -O2 -ffp-contract=off -fno-fast-math -fcx-limited-range (the last
+ * drops only the NaN/Inf recovery path of complex multiplication, which finite
+ * inputs never take).
  */
 #include <cmath>
 #include <complex>
@@ -210,6 +215,13 @@ void orc_spread(int64_t Np, const double* x, const double* y, const double* z,
     cplx* grid = reinterpret_cast<cplx*>(grid_out);
     const cplx* cc = reinterpret_cast<const cplx*>(c);
     std::memset(grid_out, 0, sizeof(cplx) * (size_t)(nf1 * nf2 * nf3));
+    /* z stencil start of every point (a_3 = ceil(s_3 - w/2), the same expression
+     * stencil_1d uses), so each thread can find the points that reach its planes
+     * without evaluating weights for the others.                                 */
+    std::vector<int64_t> a3v((size_t)Np);
+#pragma omp parallel for schedule(static)
+    for (int64_t j = 0; j < Np; ++j)
+        a3v[(size_t)j] = (int64_t)std::ceil(fold_rescale(z[j], L, nf3) - 0.5 * (double)w);
 #pragma omp parallel
     {
         int nth = 1, tid = 0;
@@ -219,28 +231,32 @@ void orc_spread(int64_t Np, const double* x, const double* y, const double* z,
 #endif
         int64_t z0 = nf3 * tid / nth, z1 = nf3 * (tid + 1) / nth;   /* owned planes */
         std::vector<double> w1(w), w2(w), w3(w);
+        std::vector<int64_t> m1(w), m2(w), m3(w);                    /* wrapped node indices */
         for (int64_t j = 0; j < Np; ++j) {
-            double s3 = fold_rescale(z[j], L, nf3);
-            int64_t a3 = stencil_1d(s3, w, beta, w3.data());
+            /* does [a3, a3 + w) meet the owned planes, periodically?  (a3 lies in
+             * [-w, nf3), so shifts by -nf3, 0, +nf3 cover every wrap)            */
+            int64_t lo = a3v[(size_t)j], hi = lo + w;
             bool hit = false;
-            for (int i3 = 0; i3 < w; ++i3) {
-                int64_t m3 = wrap(a3 + i3, nf3);
-                if (m3 >= z0 && m3 < z1) hit = true;
-            }
+            for (int64_t sh = -nf3; sh <= nf3; sh += nf3)
+                if (lo < z1 + sh && hi > z0 + sh) hit = true;
             if (!hit) continue;
             double s1 = fold_rescale(x[j], L, nf1);
             double s2 = fold_rescale(y[j], L, nf2);
+            double s3 = fold_rescale(z[j], L, nf3);
             int64_t a1 = stencil_1d(s1, w, beta, w1.data());
             int64_t a2 = stencil_1d(s2, w, beta, w2.data());
+            int64_t a3 = stencil_1d(s3, w, beta, w3.data());
+            for (int i = 0; i < w; ++i) {
+                m1[i] = wrap(a1 + i, nf1);
+                m2[i] = wrap(a2 + i, nf2);
+                m3[i] = wrap(a3 + i, nf3);
+            }
             for (int i3 = 0; i3 < w; ++i3) {
-                int64_t m3 = wrap(a3 + i3, nf3);
-                if (m3 < z0 || m3 >= z1) continue;
+                if (m3[i3] < z0 || m3[i3] >= z1) continue;
                 for (int i2 = 0; i2 < w; ++i2) {
-                    int64_t m2 = wrap(a2 + i2, nf2);
-                    for (int i1 = 0; i1 < w; ++i1) {
-                        int64_t m1 = wrap(a1 + i1, nf1);
-                        grid[m1 + nf1 * (m2 + nf2 * m3)] += cc[j] * (w1[i1] * w2[i2] * w3[i3]);
-                    }
+                    cplx* row = grid + nf1 * (m2[i2] + nf2 * m3[i3]);
+                    for (int i1 = 0; i1 < w; ++i1)
+                        row[m1[i1]] += cc[j] * (w1[i1] * w2[i2] * w3[i3]);
                 }
             }
         }
@@ -259,20 +275,23 @@ void orc_interp(int64_t Np, const double* x, const double* y, const double* z,
 #pragma omp parallel
     {
         std::vector<double> w1(w), w2(w), w3(w);
+        std::vector<int64_t> m1(w), m2(w), m3(w);                    /* wrapped node indices */
 #pragma omp for schedule(static)
         for (int64_t j = 0; j < Np; ++j) {
             int64_t a1 = stencil_1d(fold_rescale(x[j], L, nf1), w, beta, w1.data());
             int64_t a2 = stencil_1d(fold_rescale(y[j], L, nf2), w, beta, w2.data());
             int64_t a3 = stencil_1d(fold_rescale(z[j], L, nf3), w, beta, w3.data());
+            for (int i = 0; i < w; ++i) {
+                m1[i] = wrap(a1 + i, nf1);
+                m2[i] = wrap(a2 + i, nf2);
+                m3[i] = wrap(a3 + i, nf3);
+            }
             cplx acc(0.0, 0.0);
             for (int i3 = 0; i3 < w; ++i3) {
-                int64_t m3 = wrap(a3 + i3, nf3);
                 for (int i2 = 0; i2 < w; ++i2) {
-                    int64_t m2 = wrap(a2 + i2, nf2);
-                    for (int i1 = 0; i1 < w; ++i1) {
-                        int64_t m1 = wrap(a1 + i1, nf1);
-                        acc += grid[m1 + nf1 * (m2 + nf2 * m3)] * (w1[i1] * w2[i2] * w3[i3]);
-                    }
+                    const cplx* row = grid + nf1 * (m2[i2] + nf2 * m3[i3]);
+                    for (int i1 = 0; i1 < w; ++i1)
+                        acc += row[m1[i1]] * (w1[i1] * w2[i2] * w3[i3]);
                 }
             }
             out[j] = acc;
@@ -458,15 +477,36 @@ int orc_type2(int64_t Np, const double* x, const double* y, const double* z, con
  * directly with cos/sin (no recurrence).  If sel != NULL only the nsel modes with
  * flat indices sel[k] are evaluated, into fk_out[k]; else all N1 N2 N3 modes.
  * ------------------------------------------------------------------------- */
-static void phase_table(int64_t n, const double* x, int64_t N, int iflag, double L,
-                        std::vector<cplx>& e) {
-    e.resize((size_t)(n * N));
+static void phase_table(int64_t n, const double* x, int64_t N, const std::vector<int64_t>& idx,
+                        int iflag, double L, std::vector<cplx>& e) {
+    /* e[j K + k] = exp(iflag i (2 pi / L) n x_j) for the K centered mode indices
+     * n = idx[k] - N/2 (idx = 0..N-1 for the full table).                       */
+    int64_t K = (int64_t)idx.size();
+    e.resize((size_t)(n * K));
 #pragma omp parallel for schedule(static)
     for (int64_t j = 0; j < n; ++j)
-        for (int64_t i = 0; i < N; ++i) {
-            double ang = (double)iflag * (2.0 * kPi / L) * (double)(i - N / 2) * x[j];
-            e[(size_t)(j * N + i)] = cplx(std::cos(ang), std::sin(ang));
+        for (int64_t k = 0; k < K; ++k) {
+            double ang = (double)iflag * (2.0 * kPi / L) * (double)(idx[(size_t)k] - N / 2) * x[j];
+            e[(size_t)(j * K + k)] = cplx(std::cos(ang), std::sin(ang));
         }
+}
+
+/* Distinct per-axis indices used by the requested modes, and each mode's column in
+ * the per-axis phase table (so a sampled NUDFT evaluates only the phases it needs). */
+static void axis_columns(int64_t nout, const int64_t* sel, int64_t N, int64_t stride,
+                         std::vector<int64_t>& idx, std::vector<int64_t>& col) {
+    std::vector<int64_t> where((size_t)N, -1);
+    idx.clear();
+    col.assign((size_t)nout, 0);
+    for (int64_t k = 0; k < nout; ++k) {
+        int64_t flat = sel ? sel[k] : k;
+        int64_t i = (flat / stride) % N;
+        if (where[(size_t)i] < 0) {
+            where[(size_t)i] = (int64_t)idx.size();
+            idx.push_back(i);
+        }
+        col[(size_t)k] = where[(size_t)i];
+    }
 }
 
 void orc_nudft1(int64_t Np, const double* x, const double* y, const double* z,
@@ -477,22 +517,26 @@ void orc_nudft1(int64_t Np, const double* x, const double* y, const double* z,
     int sgn = iflag >= 0 ? 1 : -1;
     int64_t nout = sel ? nsel : N1 * N2 * N3;
     for (int64_t k = 0; k < nout; ++k) fk[k] = cplx(0.0, 0.0);
+    std::vector<int64_t> idx1, idx2, idx3, col1, col2, col3;
+    axis_columns(nout, sel, N1, 1, idx1, col1);
+    axis_columns(nout, sel, N2, N1, idx2, col2);
+    axis_columns(nout, sel, N3, N1 * N2, idx3, col3);
+    int64_t K1 = (int64_t)idx1.size(), K2 = (int64_t)idx2.size(), K3 = (int64_t)idx3.size();
     /* points in chunks so the phase tables stay small; sum over j in index order */
-    const int64_t chunk = 16384;
+    const int64_t chunk = 2048;
     std::vector<cplx> e1, e2, e3;
     for (int64_t j0 = 0; j0 < Np; j0 += chunk) {
         int64_t n = Np - j0 < chunk ? Np - j0 : chunk;
-        phase_table(n, x + j0, N1, sgn, L, e1);
-        phase_table(n, y + j0, N2, sgn, L, e2);
-        phase_table(n, z + j0, N3, sgn, L, e3);
+        phase_table(n, x + j0, N1, idx1, sgn, L, e1);
+        phase_table(n, y + j0, N2, idx2, sgn, L, e2);
+        phase_table(n, z + j0, N3, idx3, sgn, L, e3);
 #pragma omp parallel for schedule(dynamic, 16)
         for (int64_t k = 0; k < nout; ++k) {
-            int64_t flat = sel ? sel[k] : k;
-            int64_t i1 = flat % N1, i2 = (flat / N1) % N2, i3 = flat / (N1 * N2);
+            int64_t c1 = col1[(size_t)k], c2 = col2[(size_t)k], c3 = col3[(size_t)k];
             cplx acc(0.0, 0.0);
             for (int64_t j = 0; j < n; ++j)
-                acc += cc[j0 + j] * e1[(size_t)(j * N1 + i1)] * e2[(size_t)(j * N2 + i2)] *
-                       e3[(size_t)(j * N3 + i3)];
+                acc += cc[j0 + j] * e1[(size_t)(j * K1 + c1)] * e2[(size_t)(j * K2 + c2)] *
+                       e3[(size_t)(j * K3 + c3)];
             fk[k] += acc;
         }
     }
@@ -535,6 +579,42 @@ void orc_nudft2(int64_t Np, const double* x, const double* y, const double* z,
                 }
             out[k] = acc;
         }
+    }
+}
+
+/* O-NUDFT type 2, Eq. (2), for a rank-one (separable) mode array
+ *   fk[n1, n2, n3] = a1[n1] a2[n2] a3[n3]:
+ * the triple sum factors exactly into three 1D sums,
+ *   c_j = A1(x_j) A2(y_j) A3(z_j),  A_d(t) = sum_n a_d[n] exp(-iflag i (2 pi / L) n t),
+ * so the exact type-2 sum at a point costs O(N1 + N2 + N3) instead of O(N1 N2 N3)
+ * (used to check full-size configurations, where the triple sum is out of reach).
+ * a_d are centered (index n + N_d/2).  If sel != NULL only points sel[k].          */
+void orc_nudft2_separable(int64_t Np, const double* x, const double* y, const double* z,
+                          const double* a1_in, const double* a2_in, const double* a3_in,
+                          int64_t N1, int64_t N2, int64_t N3, int iflag, double L,
+                          int64_t nsel, const int64_t* sel, double* c_out) {
+    const cplx* a1 = reinterpret_cast<const cplx*>(a1_in);
+    const cplx* a2 = reinterpret_cast<const cplx*>(a2_in);
+    const cplx* a3 = reinterpret_cast<const cplx*>(a3_in);
+    cplx* out = reinterpret_cast<cplx*>(c_out);
+    int sgn = iflag >= 0 ? -1 : 1;
+    int64_t nout = sel ? nsel : Np;
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t k = 0; k < nout; ++k) {
+        int64_t j = sel ? sel[k] : k;
+        const double* t[3] = {x, y, z};
+        const cplx* a[3] = {a1, a2, a3};
+        int64_t N[3] = {N1, N2, N3};
+        cplx prod(1.0, 0.0);
+        for (int d = 0; d < 3; ++d) {
+            cplx acc(0.0, 0.0);
+            for (int64_t i = 0; i < N[d]; ++i) {
+                double ang = (double)sgn * (2.0 * kPi / L) * (double)(i - N[d] / 2) * t[d][j];
+                acc += a[d][i] * cplx(std::cos(ang), std::sin(ang));
+            }
+            prod *= acc;
+        }
+        out[k] = prod;
     }
 }
 

@@ -261,6 +261,50 @@ def test_nudft_one_particle_and_sampling():
     assert np.array_equal(oracle.nudft2(x, y, z, fk, sel=[3, 0, 39]), full2[[3, 0, 39]])
 
 
+def test_nudft_sampled_modes_span_point_chunks():
+    # sampled modes on a tensor product of per-axis indices (the full-size parity
+    # tests' layout), with more points than one phase-table chunk: identical to
+    # the full evaluation at those modes
+    N = (8, 6, 10)
+    x, y, z = _pts(5000, seed=11)
+    c = _c(5000, seed=12)
+    full = oracle.nudft1(x, y, z, c, N)
+    ax = [np.array([0, 3, 7]), np.array([1, 5]), np.array([0, 4, 9])]
+    sel = ((ax[2][:, None, None] * N[1] + ax[1][None, :, None]) * N[0]
+           + ax[0][None, None, :]).ravel()
+    assert np.array_equal(oracle.nudft1(x, y, z, c, N, sel=sel), full.ravel()[sel])
+
+
+def test_nudft2_separable_equals_fft_and_triple_sum():
+    # rank-one modes fk[n3, n2, n1] = a1[n1] a2[n2] a3[n3]: on grid-aligned points
+    # Eq. (2) is an inverse DFT (numpy.fft); at random points it equals the
+    # general triple sum orc_nudft2
+    N = (8, 6, 4)
+    rng = np.random.default_rng(8)
+    a = [rng.standard_normal(n) + 1j * rng.standard_normal(n) for n in N]
+    fk = np.einsum("k,j,i->kji", a[2], a[1], a[0])
+    m = [rng.integers(0, n, 300) for n in N]
+    x, y, z = (m[d] * (TWO_PI / N[d]) for d in range(3))
+    G = np.fft.ifftn(np.fft.ifftshift(fk)) * fk.size
+    ref = G[m[2], m[1], m[0]]
+    got = oracle.nudft2_separable(x, y, z, *a, iflag=-1)
+    assert np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref))
+    xr, yr, zr = _pts(500, seed=13)
+    for iflag in (-1, 1):
+        tri = oracle.nudft2(xr, yr, zr, fk, iflag=iflag)
+        sep = oracle.nudft2_separable(xr, yr, zr, *a, iflag=iflag)
+        assert oracle.rel_l2(sep, tri) <= 1e-13
+    sel = np.array([499, 0, 17])
+    assert np.array_equal(oracle.nudft2_separable(xr, yr, zr, *a, sel=sel),
+                          oracle.nudft2_separable(xr, yr, zr, *a)[sel])
+
+
+def test_max_abs_error_helper():
+    b = np.array([1.0, -4.0, 2.0j])
+    assert oracle.max_abs(b, b) == 0.0
+    assert oracle.max_abs(b + np.array([0, 0.5, 0]), b) == 0.5 / 4.0
+
+
 # ---------------------------------------------------------------- NUFFT vs NUDFT
 @pytest.mark.parametrize("eps", [1e-2, 1e-3, 1e-4, 1e-6, 1e-8, 1e-10])
 def test_type1_type2_within_10eps_of_nudft(eps):
