@@ -125,7 +125,10 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
  * them by tile (counting sort with warp-level prefix scans), store sorted per-point
  * stencil records.  x, y, z: Np reals each of the plan precision, device or host.
  * Distributed plans: collective over the communicator; points are redistributed
- * to their owning z-slab unless opts.points_owned (blocks the host for the counts). */
+ * to their owning z-slab unless opts.points_owned (blocks the host for the counts).
+ * A local failure (allocation, >= 2^31 points arriving on one rank) is agreed by an
+ * all-reduce before any point moves: the failing rank returns its own code, every
+ * other rank NUFFT_ERR_NCCL, and no rank is left waiting in the exchange. */
 int nufft_setpts(nufft_handle h, int64_t Np, const void* x, const void* y, const void* z);
 
 /* Type-1 NUFFT (Eq. 3): c = Np complex strengths (caller order), fk = N1 N2 N3 complex out.
@@ -172,6 +175,14 @@ int nufft_destroy(nufft_handle h);
 
 /* Plan parameters and, with opts.timing, the last per-stage device times.  Blocks. */
 int nufft_get_info(nufft_handle h, nufft_info* info);
+
+/* Diagnostics (not a step of the method): the measured FMA-pipe peak of this GPU in
+ * TFLOP/s (2 flops per FMA) for precision NUFFT_F32 / NUFFT_F64 -- the ALU roofline
+ * denominator of bench.py ("measure on the box with an FMA
+ * microbenchmark").  8 independent FMA chains per thread, 8 CTAs of 256 threads per SM,
+ * CUDA-event timed on `stream` (cudaStream_t, NULL = default).  Blocks the host.
+ * *tflops is host memory.  NUFFT_ERR_ARG for a bad precision / NULL tflops. */
+int nufft_fma_peak(int precision, void* stream, double* tflops);
 
 /* Static string for a status code (host). */
 const char* nufft_strerror(int code);
@@ -223,9 +234,11 @@ int nufft_pif_drift(nufft_handle h, int64_t Np, void* x, void* y, void* z, const
  * device arrays of capacity cap >= *np).  Every particle whose fine z-cell lies outside
  * this rank's slab is sent to its owner (NCCL send/recv of the leavers only); the staying
  * particles are compacted into [0, *np - leavers) in place (their order may change) and
- * the arrivals appended.  Out: *np = the new local count.  NUFFT_ERR_NPTS on EVERY rank
- * if the new count of any rank would exceed its cap (agreed collectively before anything
- * moves: all particles stay where they were).  On a one-GPU plan: no-op. */
+ * the arrivals appended.  Out: *np = the new local count.  An error on EVERY rank if any
+ * rank's new count would exceed its cap or its staging allocation fails (agreed
+ * collectively before anything moves, all particles stay where they were):
+ * NUFFT_ERR_NPTS, or NUFFT_ERR_ALLOC on the rank whose allocation failed.  On a one-GPU
+ * plan: no-op. */
 int nufft_pif_migrate(nufft_handle h, int64_t* np, int64_t cap, void* x, void* y, void* z,
                       void* vx, void* vy, void* vz);
 

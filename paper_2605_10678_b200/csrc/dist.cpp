@@ -452,6 +452,22 @@ int dist_local_modes(nufft_plan_s* p, int64_t lo[3], int64_t hi[3]) {
     return NUFFT_OK;
 }
 
+// Collective agreement on a local status before an exchange: every rank learns
+// whether ANY rank failed (allocation, size check), and all of them return an
+// error together -- no rank is left waiting in a later ncclSend / ncclRecv.  A
+// rank that did not fail itself reports NUFFT_ERR_NCCL ("a peer failed").
+static int agree(nufft_plan_s* p, int local) {
+    DistState* d = p->dist;
+    unsigned long long flag = local >= 2 ? 1ull : 0ull;
+    unsigned long long* f = d->d_mig + d->P + 2;
+    NUFFT_CK(cudaMemcpyAsync(f, &flag, sizeof(flag), cudaMemcpyHostToDevice, p->stream));
+    NCK(ncclAllReduce(f, f, 1, ncclUint64, ncclMax, d->nccl, p->stream));
+    NUFFT_CK(cudaMemcpyAsync(&flag, f, sizeof(flag), cudaMemcpyDeviceToHost, p->stream));
+    NUFFT_CK(cudaStreamSynchronize(p->stream));
+    if (local >= 2) return local;
+    return flag ? NUFFT_ERR_NCCL : NUFFT_OK;
+}
+
 int dist_setpts(nufft_plan_s* p, int64_t Np, const void* x, const void* y, const void* z) {
     DistState* d = p->dist;
     if (p->points_owned) {
@@ -464,15 +480,17 @@ int dist_setpts(nufft_plan_s* p, int64_t Np, const void* x, const void* y, const
     const int P = d->P;
     const size_t rs = p->real_size;
     // ---- owners and per-destination counts
+    st = NUFFT_OK;
     if (Np > d->cap_user) {
         dev_free(p, (void**)&d->owner, 4 * d->cap_user);
         dev_free(p, (void**)&d->rank_in, 4 * d->cap_user);
         d->cap_user = 0;
         const int64_t cap = Np + Np / 8;
-        if ((st = dev_alloc(p, (void**)&d->owner, 4 * (size_t)cap))) return st;
-        if ((st = dev_alloc(p, (void**)&d->rank_in, 4 * (size_t)cap))) return st;
-        d->cap_user = cap;
+        st = dev_alloc(p, (void**)&d->owner, 4 * (size_t)cap);
+        if (!st) st = dev_alloc(p, (void**)&d->rank_in, 4 * (size_t)cap);
+        if (!st) d->cap_user = cap;
     }
+    if ((st = agree(p, st))) return st;  // before the count all-to-all
     NUFFT_CK(cudaMemsetAsync(d->d_counts, 0, sizeof(unsigned long long) * P, p->stream));
     const Geom& g = p->geom;
     if (p->prec == NUFFT_F64)
@@ -498,16 +516,20 @@ int dist_setpts(nufft_plan_s* p, int64_t Np, const void* x, const void* y, const
     }
     d->np_user = Np;
     d->np_local = (int64_t)ro;
-    if (d->np_local >= (int64_t)1 << 31) return NUFFT_ERR_NPTS;
+    // ---- size check and staging buffers, agreed by every rank before any point moves
+    st = d->np_local >= (int64_t)1 << 31 ? NUFFT_ERR_NPTS : NUFFT_OK;
+    const size_t need_s = 3 * (size_t)Np * rs + 16, need_r = 3 * (size_t)d->np_local * rs + 16;
+    if (!st) st = ensure(p, &d->sbuf, &d->sbuf_bytes, std::max(need_s, (size_t)Np * p->cplx_size + 16));
+    if (!st)
+        st = ensure(p, &d->rbuf, &d->rbuf_bytes,
+                    std::max(need_r, (size_t)d->np_local * p->cplx_size + 16));
+    if ((st = agree(p, st))) {
+        d->np_local = 0;
+        return st;
+    }
     NUFFT_CK(cudaMemcpyAsync(d->d_off, d->soff.data(), sizeof(unsigned long long) * P,
                              cudaMemcpyHostToDevice, p->stream));
     // ---- move x, y, z (three rounds through the staging buffers)
-    const size_t need_s = 3 * (size_t)Np * rs + 16, need_r = 3 * (size_t)d->np_local * rs + 16;
-    if ((st = ensure(p, &d->sbuf, &d->sbuf_bytes, std::max(need_s, (size_t)Np * p->cplx_size + 16))))
-        return st;
-    if ((st = ensure(p, &d->rbuf, &d->rbuf_bytes,
-                     std::max(need_r, (size_t)d->np_local * p->cplx_size + 16))))
-        return st;
     const void* src[3] = {x, y, z};
     for (int k = 0; k < 3; ++k) {
         char* sb = static_cast<char*>(d->sbuf) + (size_t)k * Np * rs;
@@ -527,8 +549,9 @@ int dist_setpts(nufft_plan_s* p, int64_t Np, const void* x, const void* y, const
     }
     NCK(ncclGroupEnd());
     const char* rb = static_cast<const char*>(d->rbuf);
-    return local_sort(p, d->np_local, rb, rb + (size_t)d->np_local * rs,
-                      rb + 2 * (size_t)d->np_local * rs);
+    st = local_sort(p, d->np_local, rb, rb + (size_t)d->np_local * rs,
+                    rb + 2 * (size_t)d->np_local * rs);
+    return agree(p, st);  // later executes exchange again: fail together here
 }
 
 int dist_type1(nufft_plan_s* p, const void* c, void* fk) {
@@ -695,23 +718,13 @@ int migrate_t(nufft_plan_s* p, int64_t* np, int64_t cap, T* const st[6]) {
         ro += d->rcount[q];
     }
     const int64_t nleave = (int64_t)so, nrecv = (int64_t)ro;
-    // every rank must agree before any particle moves: a rank without room fails
-    // the call on ALL ranks (no rank may be left waiting in the exchange)
-    {
-        unsigned long long flag = (n - nleave + nrecv > cap) ? 1ull : 0ull;
-        NUFFT_CK(cudaMemcpyAsync(d->d_mig + P + 2, &flag, sizeof(flag), cudaMemcpyHostToDevice,
-                                 p->stream));
-        NCK(ncclAllReduce(d->d_mig + P + 2, d->d_mig + P + 2, 1, ncclUint64, ncclMax, d->nccl,
-                          p->stream));
-        NUFFT_CK(cudaMemcpyAsync(&flag, d->d_mig + P + 2, sizeof(flag), cudaMemcpyDeviceToHost,
-                                 p->stream));
-        NUFFT_CK(cudaStreamSynchronize(p->stream));
-        if (flag) return NUFFT_ERR_NPTS;  // state untouched on every rank
-    }
-    int s;
-    if ((s = ensure(p, &d->mig_send, &d->mig_send_bytes, 6 * (size_t)nleave * rs + 16))) return s;
-    if ((s = ensure(p, &d->mig_recv, &d->mig_recv_bytes, 6 * (size_t)nrecv * rs + 16))) return s;
-    if ((s = ensure(p, &d->mig_idx, &d->mig_idx_bytes, 3 * (size_t)nleave * 8 + 16))) return s;
+    // every rank must agree before any particle moves: a rank without room (or
+    // without staging memory) fails the call on ALL ranks, state untouched
+    int s = (n - nleave + nrecv > cap) ? NUFFT_ERR_NPTS : NUFFT_OK;
+    if (!s) s = ensure(p, &d->mig_send, &d->mig_send_bytes, 6 * (size_t)nleave * rs + 16);
+    if (!s) s = ensure(p, &d->mig_recv, &d->mig_recv_bytes, 6 * (size_t)nrecv * rs + 16);
+    if (!s) s = ensure(p, &d->mig_idx, &d->mig_idx_bytes, 3 * (size_t)nleave * 8 + 16);
+    if ((s = agree(p, s))) return s == NUFFT_ERR_NCCL ? NUFFT_ERR_NPTS : s;
     NUFFT_CK(cudaMemcpyAsync(d->d_off, d->soff.data(), sizeof(unsigned long long) * P,
                              cudaMemcpyHostToDevice, p->stream));
     NUFFT_CK(cudaMemsetAsync(d->d_mig, 0, sizeof(unsigned long long) * (P + 2), p->stream));

@@ -50,12 +50,11 @@ int select_width(double eps, int precision, int* w, double* beta, double* eps_us
 // phihat(xi) = int_{-1}^{1} exp(beta (sqrt(1 - z^2) - 1)) cos(xi z) dz
 // (PAPER.md:178-179), evaluated on theta = asin(z) with a 100-node
 // Gauss-Legendre rule whose nodes come from std::legendre + Newton.
-double es_phihat(double xi, double beta) {
-    static std::vector<double> nodes, weights;
-    const int n = 100;
-    if (nodes.empty()) {
-        nodes.resize(n);
-        weights.resize(n);
+namespace {
+struct GaussLegendre100 {
+    static constexpr int n = 100;
+    double nodes[n], weights[n];
+    GaussLegendre100() {
         for (int k = 0; k < n; ++k) {
             double t = std::cos(M_PI * (k + 0.75) / (n + 0.5));
             double dp = 1.0;
@@ -72,6 +71,16 @@ double es_phihat(double xi, double beta) {
             weights[k] = 2.0 / ((1.0 - t * t) * dp * dp);
         }
     }
+};
+}  // namespace
+
+double es_phihat(double xi, double beta) {
+    // built once, thread-safely (C++11 magic static): plans may be created
+    // concurrently from several host threads (one per GPU)
+    static const GaussLegendre100 gl;
+    const int n = GaussLegendre100::n;
+    const double* nodes = gl.nodes;
+    const double* weights = gl.weights;
     const double h = 0.5 * M_PI;
     double acc = 0.0;
     for (int k = 0; k < n; ++k) {
@@ -407,22 +416,19 @@ static const void* interp_tmap(nufft_plan_s* p, const void* grid0) {
                                 const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                 const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                 CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-    static Encode encode = nullptr;
-    static int resolved = 0;
-    if (p->tmap_state < 0 || grid0 == nullptr) return nullptr;
-    if (p->tmap_state == 1 && p->tmap_grid == grid0) return p->tmap;
-    if (!resolved) {
+    // resolved once, thread-safely; NUFFT_NO_TMAP=1 is the ablation switch
+    // (profiles/README.md)
+    static const Encode encode = []() -> Encode {
+        if (std::getenv("NUFFT_NO_TMAP")) return nullptr;
         void* fn = nullptr;
-        if (std::getenv("NUFFT_NO_TMAP")) {  // ablation switch (profiles/README.md)
-            resolved = 1;
-            return nullptr;
-        }
         cudaDriverEntryPointQueryResult q;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
                 cudaSuccess && q == cudaDriverEntryPointSuccess)
-            encode = reinterpret_cast<Encode>(fn);
-        resolved = 1;
-    }
+            return reinterpret_cast<Encode>(fn);
+        return nullptr;
+    }();
+    if (p->tmap_state < 0 || grid0 == nullptr) return nullptr;
+    if (p->tmap_state == 1 && p->tmap_grid == grid0) return p->tmap;
     const int w = p->w, r = (int)p->real_size;
     const int pitch = interp_tile_pitch(2 * r, p->geom.T[0], w);
     const cuuint64_t dim[3] = {(cuuint64_t)(2 * p->nf[0]), (cuuint64_t)p->nf[1],
@@ -432,17 +438,22 @@ static const void* interp_tmap(nufft_plan_s* p, const void* grid0) {
     const cuuint32_t box[3] = {(cuuint32_t)(2 * pitch), (cuuint32_t)(p->geom.T[1] + w),
                                (cuuint32_t)(p->geom.T[2] + w)};
     const cuuint32_t estride[3] = {1, 1, 1};
+    // plan-level impossibility (no driver entry point, box or pitch out of range):
+    // latch TMA staging off for this plan
     if (!encode || box[0] > 256 || box[1] > 256 || box[2] > 256 || (box[0] * r) % 16 ||
-        (stride[0] % 16) || (reinterpret_cast<uintptr_t>(grid0) % 16)) {
+        (stride[0] % 16)) {
         p->tmap_state = -1;
         return nullptr;
     }
+    // per-grid failure (a misaligned caller grid, an encode refused for this address):
+    // stage this call row by row, keep TMA for later grids
+    if (reinterpret_cast<uintptr_t>(grid0) % 16) return nullptr;
     if (encode(reinterpret_cast<CUtensorMap*>(p->tmap),
                r == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
                const_cast<void*>(grid0), dim, stride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
-        p->tmap_state = -1;
+        if (p->tmap_state == 1) p->tmap_state = 0;  // the cached map belongs to another grid
         return nullptr;
     }
     p->tmap_state = 1;

@@ -49,12 +49,10 @@ __global__ void __launch_bounds__(kSortThreads) bin_count_kernel(
     Geom g, int64_t Np, const T* __restrict__ x, const T* __restrict__ y,
     const T* __restrict__ z, uint32_t* __restrict__ count, uint32_t* __restrict__ bin_of,
     uint32_t* __restrict__ rank_of) {
-    const int lane = threadIdx.x & 31;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i - lane < Np;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < Np;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const bool live = i < Np;
-        uint32_t bin = 0xffffffffu;
-        if (live) {
+        uint32_t bin;
+        {
             int cx = cell_of(fold_rescale((double)x[i], g.L, g.scale[0], g.nf[0]), g.nf[0]);
             int cy = cell_of(fold_rescale((double)y[i], g.L, g.scale[1], g.nf[1]), g.nf[1]);
             int cz = cell_of(fold_rescale((double)z[i], g.L, g.scale[2], g.nf[2]), g.nf[2]) -
@@ -69,10 +67,8 @@ __global__ void __launch_bounds__(kSortThreads) bin_count_kernel(
         // aggregated __match_any_sync version was measured slower on B200 for the
         // paper's near-uniform workloads: setpts C2b 0.170 -> 0.152 ms, C3 18.0 ->
         // 16.5 ms without it; collisions inside a warp are rare at ~1e4-1e5 bins.)
-        if (live) {
-            bin_of[i] = bin;
-            rank_of[i] = atomicAdd(&count[bin], 1u);
-        }
+        bin_of[i] = bin;
+        rank_of[i] = atomicAdd(&count[bin], 1u);
     }
 }
 

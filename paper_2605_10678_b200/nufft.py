@@ -1,8 +1,11 @@
 """Thin ctypes binding of libnufft.so (include/nufft.h) -- argument marshalling only.
 
 Every step of the NUFFT runs in the library's CUDA kernels (and cuFFT).  This
-module converts torch tensors to raw pointers, passes the current CUDA stream
-and raises on non-zero status.  There is NO CPU fallback: if the shared library
+module converts torch tensors to raw pointers and raises on non-zero status.
+The plan runs on the stream current at plan creation (or ``stream=``); every
+call is ordered after the caller's CURRENT stream (its inputs are ready) and
+the caller's stream waits for the plan stream afterwards (outputs are visible),
+with the tensors recorded on the plan stream for the caching allocator.  There is NO CPU fallback: if the shared library
 is missing or CUDA is absent the calls fail loudly.
 
     import torch, paper_2605_10678_b200 as nb
@@ -13,6 +16,7 @@ is missing or CUDA is absent the calls fail loudly.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import math
 import os
@@ -63,7 +67,7 @@ _EXPORTS = ["nufft_default_opts", "nufft_plan", "nufft_setpts", "nufft_execute_t
             "nufft_comm_destroy", "nufft_local_modes", "nufft_pif_poisson", "nufft_pif_kick",
             "nufft_pif_drift", "nufft_pif_migrate", "nufft_execute_type1_real",
             "nufft_execute_type2_real", "nufft_pif_kick_real", "nufft_pif_poisson_real",
-            "nufft_execute_type2_real3", "nufft_pif_gather_kick"]
+            "nufft_execute_type2_real3", "nufft_pif_gather_kick", "nufft_fma_peak"]
 
 _lib = None
 
@@ -84,6 +88,7 @@ def lib():
                   "nufft_execute_type1_real", "nufft_execute_type2_real"):
             getattr(L, f).argtypes = [vp, vp, vp]
         L.nufft_destroy.argtypes = [vp]
+        L.nufft_fma_peak.argtypes = [ctypes.c_int, vp, ctypes.POINTER(ctypes.c_double)]
         L.nufft_get_info.argtypes = [vp, ctypes.POINTER(Info)]
         L.nufft_strerror.argtypes = [ctypes.c_int]
         L.nufft_strerror.restype = ctypes.c_char_p
@@ -147,6 +152,15 @@ class Comm:
         if getattr(self, "_h", None):
             lib().nufft_comm_destroy(self._h)
             self._h = None
+
+
+def fma_peak(precision="f64", stream=None) -> float:
+    """Measured FMA-pipe peak of the current GPU in TFLOP/s (nufft_fma_peak)."""
+    st = (stream or torch.cuda.current_stream()).cuda_stream
+    v = ctypes.c_double()
+    prec = F64 if precision in ("f64", "double", torch.float64) else F32
+    _check(lib().nufft_fma_peak(prec, ctypes.c_void_p(st), ctypes.byref(v)), "nufft_fma_peak")
+    return float(v.value)
 
 
 class Plan:
@@ -237,6 +251,21 @@ class Plan:
         self.close()
 
     # -- calls
+    @contextlib.contextmanager
+    def _call(self, *tensors):
+        """One library call on the plan stream, ordered against the caller's stream."""
+        with torch.cuda.device(self.device):
+            cur = torch.cuda.current_stream(self.device)
+            other = cur.cuda_stream != self._stream.cuda_stream
+            if other:
+                self._stream.wait_stream(cur)
+            yield
+            if other:
+                for t in tensors:
+                    if isinstance(t, torch.Tensor) and t.is_cuda:
+                        t.record_stream(self._stream)
+                cur.wait_stream(self._stream)
+
     def info(self) -> dict:
         i = Info()
         _check(lib().nufft_get_info(self._h, ctypes.byref(i)), "nufft_get_info")
@@ -247,7 +276,7 @@ class Plan:
         px = _ptr(x, self.real, n, "x")
         py = _ptr(y, self.real, n, "y")
         pz = _ptr(z, self.real, n, "z")
-        with torch.cuda.device(self.device):
+        with self._call(x, y, z):
             _check(lib().nufft_setpts(self._h, n, px, py, pz), "nufft_setpts")
         self.Np = n
         return self
@@ -263,7 +292,7 @@ class Plan:
         fk = self._out(out, self.local_shape, c)
         pc = _ptr(c, self.cplx, self.Np, "c")
         pf = _ptr(fk, self.cplx, math.prod(self.local_shape), "fk")
-        with torch.cuda.device(self.device):
+        with self._call(c, fk):
             _check(lib().nufft_execute_type1(self._h, pc, pf), "nufft_execute_type1")
         return fk
 
@@ -271,7 +300,7 @@ class Plan:
         c = self._out(out, (self.Np,), fk)
         pf = _ptr(fk, self.cplx, math.prod(self.local_shape), "fk")
         pc = _ptr(c, self.cplx, self.Np, "c")
-        with torch.cuda.device(self.device):
+        with self._call(fk, c):
             _check(lib().nufft_execute_type2(self._h, pf, pc), "nufft_execute_type2")
         return c
 
@@ -280,7 +309,7 @@ class Plan:
         fk = self._out(out, self.local_shape_real, c)
         pc = _ptr(c, self.real, self.Np, "c")
         pf = _ptr(fk, self.cplx, math.prod(self.local_shape_real), "fk")
-        with torch.cuda.device(self.device):
+        with self._call(c, fk):
             _check(lib().nufft_execute_type1_real(self._h, pc, pf), "nufft_execute_type1_real")
         return fk
 
@@ -292,7 +321,7 @@ class Plan:
                               pin_memory=(dev.type == "cpu" and torch.cuda.is_available()))
         pf = _ptr(fk, self.cplx, math.prod(self.local_shape_real), "fk")
         pc = _ptr(out, self.real, self.Np, "c")
-        with torch.cuda.device(self.device):
+        with self._call(fk, out):
             _check(lib().nufft_execute_type2_real(self._h, pf, pc), "nufft_execute_type2_real")
         return out
 
@@ -304,7 +333,7 @@ class Plan:
         n = math.prod(self.local_shape_real)
         ps = [_ptr(f, self.cplx, n, "fk") for f in (fk0, fk1, fk2)]
         pc = _ptr(out, self.real, 3 * self.Np, "c")
-        with torch.cuda.device(self.device):
+        with self._call(fk0, fk1, fk2, out):
             _check(lib().nufft_execute_type2_real3(self._h, *ps, pc), "nufft_execute_type2_real3")
         return out
 
@@ -313,7 +342,7 @@ class Plan:
         g = self._out(out, (2 * N3, 2 * N2, 2 * N1), c)
         pc = _ptr(c, self.cplx, self.Np, "c")
         pg = _ptr(g, self.cplx, 8 * N1 * N2 * N3, "grid")
-        with torch.cuda.device(self.device):
+        with self._call(c, g):
             _check(lib().nufft_spread(self._h, pc, pg), "nufft_spread")
         return g
 
@@ -322,6 +351,6 @@ class Plan:
         c = self._out(out, (self.Np,), grid)
         pg = _ptr(grid, self.cplx, 8 * N1 * N2 * N3, "grid")
         pc = _ptr(c, self.cplx, self.Np, "c")
-        with torch.cuda.device(self.device):
+        with self._call(grid, c):
             _check(lib().nufft_interp(self._h, pg, pc), "nufft_interp")
         return c

@@ -103,15 +103,17 @@ class LandauPIF:
     def migrate(self):
         """Hand particles that left this rank's slab to their owners (collective)."""
         n = ctypes.c_int64(self.Np)
-        _n._check(_n.lib().nufft_pif_migrate(self.plan._h, ctypes.byref(n), self.cap,
-                                             *(ctypes.c_void_p(a.data_ptr()) for a in self._state)),
-                  "nufft_pif_migrate")
+        with self.plan._call():
+            _n._check(_n.lib().nufft_pif_migrate(self.plan._h, ctypes.byref(n), self.cap,
+                                                 *(ctypes.c_void_p(a.data_ptr())
+                                                   for a in self._state)),
+                      "nufft_pif_migrate")
         self.Np = int(n.value)
 
     def step(self):
         p, L = self.plan, _n.lib()
         n = self.Np
-        with torch.cuda.device(p.device):
+        with p._call():                      # plan stream, ordered against the caller's
             p.setpts(self.x, self.y, self.z)                                   # sort
             if self.real:
                 p.type1_real(self.charge[:n], out=self.rho_k)                  # (1) scatter
