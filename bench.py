@@ -11,15 +11,19 @@ in HBM; L2 is flushed (a 512 MB write) before every timed step, outside the
 timed events.  `e2e` is the same metric through the C ABI with pinned HOST
 buffers (H2D of x, y, z, c, fk and D2H of fk, c inside the timed region).
 
-Default workload = BASELINE.json configs[1] (C2b: fp32, 128^3 modes, 2^21
-uniform points, eps = 1e-6).  N > 1 (torchrun): the SAME workload on a z-slab
+Default workload = the metric's configuration, BASELINE.json configs[3] (C4):
+fp64, 512^3 modes, 2^30 = 1.07e9 Landau-perturbed points on [0, 4 pi)^3, eps =
+1e-4 -- the NUFFT step over the PIF particles; the line also carries the PIF
+seconds per step of the same configuration (`pif`).  `--config c2b | c3 | ...`
+selects the other BASELINE configs.  N > 1 (torchrun): the SAME workload on a z-slab
 plan over NCCL ("scaling": "strong"): each rank starts with Np/N points drawn
 over the whole domain (setpts redistributes them to their slab owners), halos
 are exchanged with the z-neighbours and the slab FFT transposes with
 ncclAlltoAll; value = all points / max-over-ranks device time per step.
 
 --impl reference: the CPU oracle (oracle/, plain C++ fp64) on the same config,
-rank 0 only, each step a bounded sample of the workload (2^19 points).
+rank 0 only, each step a bounded sample of the workload (the same point density
+and eps on a 1/64 box: 128^3 modes, 2^24 points for C4; see ref_sample()).
 """
 from __future__ import annotations
 
@@ -39,6 +43,11 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 CONFIGS = {
+    # the metric's configuration (BASELINE.json configs[3]): the
+    # 512^3-mode Landau workload as a NUFFT step -- fp64, 2^30 = 1.07e9 Landau-perturbed
+    # points on [0, 4 pi)^3 (8 per mode), eps = 1e-4.  The default bench line.
+    "c4n": dict(name="C4", prec="f64", N=(512, 512, 512), Np=8 * 512 ** 3, eps=1e-4,
+                kind="landau", L=4 * math.pi, pif="c4"),
     "c1": dict(name="C1", prec="f64", N=(32, 32, 32), Np=100_000, eps=1e-6, kind="uniform"),
     "c2a": dict(name="C2a", prec="f32", N=(128, 128, 128), Np=1 << 21, eps=1e-4, kind="uniform"),
     "c2b": dict(name="C2b", prec="f32", N=(128, 128, 128), Np=1 << 21, eps=1e-6, kind="uniform"),
@@ -182,18 +191,24 @@ def algorithmic_bytes(cfg, stage):
 
 
 def algorithmic_flops(cfg, w, real=False):
-    """Per launch of spread or interp: the tensor-product evaluation of the w^3 stencil
-    per point -- w^3 value x weight multiply-adds (4 flops complex, 2 real) plus the
-    2 w^2 + 2 w (complex) partial products of the separable weights."""
-    per = 4 * w ** 3 + 2 * w ** 2 + 2 * w
-    return cfg["Np"] * (per // 2 if real else per)
+    """Per launch of spread or interp: per point one value x weight
+    multiply-add per stencil cell -- 4 w^3 flops complex, 2 w^3 real -- plus the 3 w^2
+    products of the separable weights (the 3 w ES evaluations are not counted)."""
+    per = (2 if real else 4) * w ** 3 + 3 * w ** 2
+    return cfg["Np"] * per
 
 
-def alu_peak_tflops(prec, sm_mhz=1965.0):
-    """FMA-pipe peak from unit counts and clocks (B200_PROFILING.md: 148 SMs, 1965 MHz):
-    fp32 128 FMA lanes/clk/SM, fp64 64 (2 flops per FMA)."""
-    lanes = 128 if prec == "f32" else 64
-    return 148 * lanes * 2 * sm_mhz * 1e6 / 1e12
+_PEAK_CACHE = {}
+
+
+def alu_peak_tflops(prec):
+    """FMA-pipe peak of THIS GPU, measured by nufft_fma_peak (8 independent FMA chains
+    per thread, 8 x 256 threads per SM; the best of three runs).  The datasheet figure
+    for comparison: 148 SMs x 128 (fp32) / 64 (fp64) FMA lanes x 2 x 1965 MHz."""
+    if prec not in _PEAK_CACHE:
+        import paper_2605_10678_b200 as nb
+        _PEAK_CACHE[prec] = max(nb.fma_peak(prec) for _ in range(3))
+    return _PEAK_CACHE[prec]
 
 
 def roofline_obj(cfg, dom, dom_ms, ws, w, real, traffic):
@@ -208,19 +223,40 @@ def roofline_obj(cfg, dom, dom_ms, ws, w, real, traffic):
     tfs = flops / (dom_ms / 1e3) / 1e12 if dom_ms > 0 else 0.0
     peak = alu_peak_tflops(cfg["prec"])
     return {"kernel": dom, "bound": "alu", "achieved": tfs, "peak": peak, "unit": "TFLOP/s",
-            "frac": tfs / peak, "peak_source": "derived: 148 SM x FMA lanes x 2 x 1965 MHz "
-                                                  "(B200_PROFILING.md), DESIGN.md section 9",
+            "frac": tfs / peak,
+            "peak_source": f"measured live: nufft_fma_peak ({cfg['prec']} FMA chains, this GPU); "
+                           f"datasheet {148 * (64 if cfg['prec'] == 'f64' else 128) * 2 * 1.965e-3:.1f}",
             "traffic": traffic, "algorithmic_flops_per_launch": flops,
+            "flops_per_point": (2 if real else 4) * w ** 3 + 3 * w ** 2,
             "ms_per_launch": dom_ms,
             "hbm": {"achieved": gbs, "peak": hbm, "peak_source": peak_src, "unit": "GB/s",
                     "frac": gbs / hbm, "algorithmic_bytes_per_launch": bytes_alg}}
 
 
+def source_sha():
+    """sha256 (16 hex) of the CUDA / C++ sources of libnufft: a committed ncu traffic
+    figure is reported only while the kernels it measured are unchanged."""
+    import hashlib
+    h = hashlib.sha256()
+    d = os.path.join(ROOT, "paper_2605_10678_b200", "csrc")
+    for f in sorted(os.listdir(d)):
+        if f.endswith((".cu", ".cuh", ".h", ".cpp")):
+            with open(os.path.join(d, f), "rb") as fh:
+                h.update(f.encode() + fh.read())
+    return h.hexdigest()[:16]
+
+
 def load_traffic(cfg_key, kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu
+    capture (profiles/traffic.json), or None if the sources changed since."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(p) as f:
-            return json.load(f)[cfg_key][kernel]
+            t = json.load(f)
+        e = t[cfg_key][kernel]
+        if isinstance(e, dict):
+            return e["bytes"] if e.get("src_sha") == source_sha() else None
+        return None
     except Exception:
         return None
 
@@ -241,7 +277,7 @@ def run_ours(args, cfg):
     plan = nb.Plan(N, cfg["eps"], precision=cfg["prec"], timing=True, device=device,
                    tile=args.tile, spread_warps=args.spread_warps, comm=comm,
                    points_owned=ws > 1, interp_method=args.interp_method,
-                   precompute=args.precompute)
+                   precompute=args.precompute, L=cfg.get("L", 2 * math.pi))
     pts, c, fk = make_inputs(cfg, rank, ws, device, plan.local_modes() if ws > 1 else None)
     Np = pts[0].numel()
     if args.real:  # real strengths / outputs: the R2C / C2R path
@@ -293,19 +329,27 @@ def run_ours(args, cfg):
     ms_per_step = t_max / args.steps
     value = Np_total / (ms_per_step / 1e3)   # all ranks' points per second
 
-    # -- end to end through the C ABI with pinned host buffers
-    hp = [p.cpu().pin_memory() for p in pts]
-    hc = c.cpu().pin_memory()
-    hfk = fk.cpu().pin_memory()
-    hfk_out = torch.empty(fk.shape, dtype=fk.dtype).pin_memory()
-    hc2 = torch.empty(Np, dtype=c.dtype).pin_memory()
+    # -- end to end through the C ABI with pinned host buffers (the device copies of
+    # the inputs are released first: the plan stages host arrays in its own buffers)
+    def pinned(t):
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t)
+        return h
+    hp = [pinned(p) for p in pts]
+    hc = pinned(c)
+    hfk = pinned(fk)
+    hfk_out = torch.empty(fk.shape, dtype=fk.dtype, pin_memory=True)
+    hc2 = torch.empty(Np, dtype=c.dtype, pin_memory=True)
+    fk_shape, c_dtype, nmodes = fk.shape, c.dtype, fk.numel()
+    del pts, c, fk, c2, fk_out, flush
+    torch.cuda.empty_cache()
 
     def e2e_step():
         plan.setpts(*hp)
         t1(hc, out=hfk_out)
         t2(hfk, out=hc2)
 
-    e2e_steps = max(3, min(args.steps, 20))
+    e2e_steps = max(3, min(args.steps, 20 if Np_total <= (1 << 24) else 5))
     for _ in range(2):
         e2e_step()
     torch.cuda.synchronize()
@@ -323,7 +367,6 @@ def run_ours(args, cfg):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         te = float(t.item())
     r = 8 if cfg["prec"] == "f64" else 4
-    nmodes = fk.numel()  # this rank's mode block
     cr = 1 if args.real else 2  # reals per strength / output value
     h2d = 3 * Np * r + Np * cr * r + nmodes * 2 * r
     d2h = nmodes * 2 * r + Np * cr * r
@@ -336,6 +379,17 @@ def run_ours(args, cfg):
     med = {k: statistics.median(v) for k, v in stage.items() if v and min(v) >= 0}
     dom = "spread" if med.get("ms_spread", 0) >= med.get("ms_interp", 0) else "interp"
     dom_ms = med["ms_" + dom]
+    info = plan.info()
+    roof = roofline_obj(cfg, dom, dom_ms, ws, info["w"], args.real, load_traffic(args.config, dom))
+    plan.close()
+    del hp, hc, hfk, hfk_out, hc2
+    torch.cuda.empty_cache()
+    # the PIF seconds per step of the same configuration (BASELINE metric, 2nd part)
+    pif = None
+    if cfg.get("pif") and not args.no_pif:
+        pargs = argparse.Namespace(**vars(args))
+        pargs.steps, pargs.warmup, pargs.no_cpu_baseline = min(args.steps, 10), 3, True
+        pif = run_pif(pargs, CONFIGS[cfg["pif"]], comm=comm, inner=True)
     out = None
     if rank == 0:
         cpu = cpu_baseline(cfg) if (ws == 1 and not args.no_cpu_baseline) else None
@@ -348,11 +402,12 @@ def run_ours(args, cfg):
             "config": {"workload": f"{cfg['name']}: {cfg['prec']} {N[0]}x{N[1]}x{N[2]} modes, "
                                    f"{Np_total} {cfg['kind']} points, eps={cfg['eps']:g}",
                        "N": list(N), "Np_total": Np_total, "eps": cfg["eps"],
-                       "w": plan.info()["w"], "precision": cfg["prec"], "points": cfg["kind"],
-                       "tile": plan.info()["tile"],
+                       "L": cfg.get("L", 2 * math.pi),
+                       "w": info["w"], "precision": cfg["prec"], "points": cfg["kind"],
+                       "tile": info["tile"],
                        "kernels": {"spread_warps": args.spread_warps,
                                    "interp_method": args.interp_method,
-                                   "weights_precomputed": plan.info()["weights_precomputed"]},
+                                   "weights_precomputed": info["weights_precomputed"]},
                        "values": "real (R2C / C2R)" if args.real else "complex",
                        "parallelism": (f"z-slab x{ws} (points owned by slab, NCCL halos + "
                                        f"all-to-all)") if ws > 1 else "1 GPU",
@@ -361,53 +416,84 @@ def run_ours(args, cfg):
             "e2e": {"value": Np_total / (te / e2e_steps / 1e3), "unit": "points/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": te / e2e_steps},
-            "gpu_launches": kernels_per_step(plan.info(), ws) * args.steps,
-            "roofline": roofline_obj(cfg, dom, dom_ms, ws, plan.info()["w"], args.real,
-                                     load_traffic(args.config, dom)),
+            "gpu_launches": kernels_per_step(info, ws) * args.steps,
+            "roofline": roof,
             "clocks": clocks,
             "cpu_baseline": cpu,
         }
-    plan.close()
+        if pif is not None:
+            out["pif"] = pif
     if ws > 1:
         comm.close()
         torch.distributed.destroy_process_group()
     return out
 
 
-def cpu_baseline(cfg, sample=REF_SAMPLE):
+def ref_sample(cfg):
+    """The bounded sample of a workload that the CPU oracle runs (cpu_baseline and the
+    --impl reference arm): workloads of <= 2^22 points keep their modes and take 2^19
+    of the points; larger ones (C3, C4) keep the point distribution, the points per mode
+    and eps on 128^3 modes (C3: 1/8, C4: 1/64 of the problem) -- the oracle's per-point
+    work is that of the full workload (same w, same density), its FFT share smaller."""
+    N, Np = cfg["N"], cfg["Np"]
+    if Np <= (1 << 22):
+        n = min(Np, REF_SAMPLE)
+        return dict(N=N, Np=n, desc=f"{n} {cfg['kind']} points of the {cfg['name']} workload "
+                                    f"({N[0]}^3 modes, eps={cfg['eps']:g})")
+    Ns = tuple(128 for _ in N)
+    n = Np * (128 ** 3) // (N[0] * N[1] * N[2])
+    return dict(N=Ns, Np=n, desc=f"the {cfg['name']} workload on a 1/{Np // n} box: {Ns[0]}^3 "
+                                 f"modes, {n} {cfg['kind']} points ({Np // (N[0] * N[1] * N[2])} "
+                                 f"per mode), eps={cfg['eps']:g}")
+
+
+def sample_inputs(cfg, smp):
+    import synthetic
+    if cfg["kind"] == "landau":
+        x, y, z = (v.numpy() for v in synthetic.landau_points(smp["Np"]))
+    else:
+        x, y, z = (v.numpy() for v in synthetic.uniform_points(smp["Np"]))
+    c = synthetic.strengths(smp["Np"]).numpy()
+    fk = synthetic.modes(*smp["N"]).numpy()
+    return x, y, z, c, fk
+
+
+def cpu_baseline(cfg):
     """The oracle as it stands, on a bounded sample of the workload, all host cores."""
     import oracle
-    import synthetic
+    smp = ref_sample(cfg)
+    L = cfg.get("L", 2 * math.pi)
     t0 = time.perf_counter()
-    x, y, z = (v.numpy() for v in synthetic.uniform_points(sample))
-    c = synthetic.strengths(sample).numpy()
-    fk = synthetic.modes(*cfg["N"]).numpy()
+    x, y, z, c, fk = sample_inputs(cfg, smp)
     t_gen = time.perf_counter() - t0
     t0 = time.perf_counter()
-    oracle.type1(x, y, z, c, cfg["N"], cfg["eps"])
-    oracle.type2(x, y, z, fk, cfg["eps"])
+    oracle.type1(x, y, z, c, smp["N"], cfg["eps"], L=L)
+    oracle.type2(x, y, z, fk, cfg["eps"], L=L)
     t = time.perf_counter() - t0
-    return {"value": sample / t, "unit": "points/s", "cores": oracle.num_threads(),
+    return {"value": smp["Np"] / t, "unit": "points/s", "cores": oracle.num_threads(),
             "kind": "oracle",
-            "sample": f"{sample} uniform points of the {cfg['name']} workload ({cfg['N'][0]}^3 "
-                      f"modes, eps={cfg['eps']:g}), one type-1 + one type-2 in fp64",
+            "sample": smp["desc"] + "; one type-1 + one type-2 in fp64 (no setpts: the oracle "
+                                    "has no sort)",
             "seconds": t, "input_gen_seconds": t_gen}
 
 
-def run_pif(args, cfg):
+def run_pif(args, cfg, comm=None, inner=False):
     """Seconds per Landau-damping PIF step: sort, type-1 charge
-    scatter, Poisson, three type-2 field gathers + kicks, drift -- all on device."""
+    scatter, Poisson, three type-2 field gathers + kicks, drift -- all on device.
+    inner=True: called from run_ours (process group and comm exist); returns the
+    compact `pif` object of the NUFFT line."""
     import paper_2605_10678_b200 as nb
     from paper_2605_10678_b200.pif import LandauPIF
     ws, rank, local = dist_env()
-    if ws > 1:
+    if ws > 1 and not inner:
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
     stream = torch.cuda.current_stream(device)
-    comm = nb.Comm() if ws > 1 else None
+    if not inner:
+        comm = nb.Comm() if ws > 1 else None
     sim = LandauPIF(cfg["N"], cfg["Np"], eps=cfg["eps"], dt=cfg["dt"], precision=cfg["prec"],
                     comm=comm, device=device, timing=True, tile=args.tile,
                     spread_warps=args.spread_warps)
@@ -460,6 +546,20 @@ def run_pif(args, cfg):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         te = float(t.item())
     med = {k: statistics.median(v) for k, v in stage.items() if v and min(v) >= 0}
+    if inner:
+        info = sim.plan.info()
+        sim.plan.close()
+        del sim
+        torch.cuda.empty_cache()
+        return {"metric": "seconds per Landau-damping PIF step", "value": ms_per_step / 1e3,
+                "unit": "s/step", "steps": args.steps, "warmup": args.warmup,
+                "higher_is_better": False,
+                "workload": f"{cfg['name']}: PIF Landau damping, {cfg['N'][0]}^3 modes, "
+                            f"{cfg['Np']} particles, eps={cfg['eps']:g}, dt={cfg['dt']}, "
+                            "real-valued transforms", "w": info["w"],
+                "stage_ms_median": med, "clocks": clocks,
+                "e2e": {"value": te / e2e_steps / 1e3, "unit": "s/step",
+                        "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 8}}
     # dominant kernel per step: spread once, interp three times
     sp, ip = med.get("ms_spread", 0.0), 3 * med.get("ms_interp", 0.0)
     dom, dom_ms = ("spread", sp) if sp >= ip else ("interp", med.get("ms_interp", 0.0))
@@ -546,14 +646,13 @@ def run_reference(args, cfg):
                 "cpu_baseline": ts[0],
                 "e2e": {"value": v, "unit": "s/step", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
-    sample = REF_SAMPLE
-    x, y, z = (v.numpy() for v in synthetic.uniform_points(sample))
-    c = synthetic.strengths(sample).numpy()
-    fk = synthetic.modes(*cfg["N"]).numpy()
+    smp = ref_sample(cfg)
+    L = cfg.get("L", 2 * math.pi)
+    x, y, z, c, fk = sample_inputs(cfg, smp)
 
     def step():
-        oracle.type1(x, y, z, c, cfg["N"], cfg["eps"])
-        oracle.type2(x, y, z, fk, cfg["eps"])
+        oracle.type1(x, y, z, c, smp["N"], cfg["eps"], L=L)
+        oracle.type2(x, y, z, fk, cfg["eps"], L=L)
 
     for _ in range(args.warmup):
         step()
@@ -561,7 +660,7 @@ def run_reference(args, cfg):
     for _ in range(args.steps):
         step()
     t = (time.perf_counter() - t0) / args.steps
-    v = sample / t
+    v = smp["Np"] / t
     N = cfg["N"]
     return {
         "impl": "reference", "metric": "NUFFT points/s (setpts + type-1 spread + type-2 interp per point)",
@@ -570,10 +669,10 @@ def run_reference(args, cfg):
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{cfg['name']}: {cfg['prec']} {N[0]}x{N[1]}x{N[2]} modes, "
                                f"{cfg['Np']} {cfg['kind']} points, eps={cfg['eps']:g}",
-                   "sample_points": sample},
+                   "sample": smp["desc"]},
         "cpu_baseline": {"value": v, "unit": "points/s", "cores": oracle.num_threads(),
                          "kind": "oracle",
-                         "sample": f"{sample} points of the workload per step (oracle type-1 + type-2, fp64)"},
+                         "sample": smp["desc"] + " per step (oracle type-1 + type-2, fp64)"},
         "e2e": {"value": v, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -583,9 +682,10 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2b", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c4n", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-pif", action="store_true", help="skip the PIF s/step key of the c4n line")
     ap.add_argument("--tile", default=None, help="bin edge T or Tx,Ty,Tz (default: built-in table)")
     ap.add_argument("--spread-warps", type=int, default=0,
                     help="spread kernel: 1 rows, 2 outer products, 4 / 8 smem planes (default: built-in)")

@@ -3,6 +3,6 @@
 The product is ``libnufft.so`` (C ABI in ``include/nufft.h``); this package is
 its thin Python binding (``nufft.py``) and its in-tree build (``build.py``).
 """
-from .nufft import F32, F64, Comm, Info, NufftError, Opts, Plan, lib, LIB_PATH  # noqa: F401
+from .nufft import F32, F64, Comm, Info, NufftError, Opts, Plan, fma_peak, lib, LIB_PATH  # noqa: F401
 
-__all__ = ["Plan", "Comm", "NufftError", "lib", "LIB_PATH", "F32", "F64"]
+__all__ = ["Plan", "Comm", "fma_peak", "NufftError", "lib", "LIB_PATH", "F32", "F64"]

@@ -12,6 +12,7 @@ import pytest
 import torch
 
 import oracle
+from errs import err
 import synthetic
 
 pytestmark = pytest.mark.gpu
@@ -69,14 +70,14 @@ def test_config1_parity_vs_oracle_and_nudft(nb, prec):
     x, y, z = (np64(p) for p in pts)
     o1 = oracle.type1(x, y, z, np64(c), N, eps)
     o2 = oracle.type2(x, y, z, np64(fk), eps)
-    assert oracle.rel_l2(g1, o1) <= TOL[prec]
-    assert oracle.rel_l2(g2, o2) <= TOL[prec]
+    assert err(g1, o1) <= TOL[prec]
+    assert err(g2, o2) <= TOL[prec]
     # accuracy vs the exact sums (sampled: 2000 modes / 2000 points)
     rng = np.random.default_rng(0)
     sm = rng.choice(np.prod(N), 2000, replace=False)
     sp = rng.choice(Np, 2000, replace=False)
-    e1 = oracle.rel_l2(g1.ravel()[sm], oracle.nudft1(x, y, z, np64(c), N, sel=sm))
-    e2 = oracle.rel_l2(g2[sp], oracle.nudft2(x, y, z, np64(fk), sel=sp))
+    e1 = err(g1.ravel()[sm], oracle.nudft1(x, y, z, np64(c), N, sel=sm))
+    e2 = err(g2[sp], oracle.nudft2(x, y, z, np64(fk), sel=sp))
     assert e1 <= 10 * eps and e2 <= 10 * eps
 
 
@@ -89,8 +90,8 @@ def test_every_width_fp64(nb, w):
     plan, g1, g2 = run_pair(nb, N, eps, "f64", pts, c, fk)
     assert plan.info()["w"] == w
     x, y, z = (np64(p) for p in pts)
-    assert oracle.rel_l2(g1, oracle.type1(x, y, z, np64(c), N, eps)) <= 1e-10
-    assert oracle.rel_l2(g2, oracle.type2(x, y, z, np64(fk), eps)) <= 1e-10
+    assert err(g1, oracle.type1(x, y, z, np64(c), N, eps)) <= 1e-10
+    assert err(g2, oracle.type2(x, y, z, np64(fk), eps)) <= 1e-10
 
 
 @pytest.mark.parametrize("w", [2, 3, 5, 7, 8])
@@ -101,8 +102,8 @@ def test_widths_fp32(nb, w):
     fk = synthetic.modes(*N).to(torch.complex64)
     plan, g1, g2 = run_pair(nb, N, eps, "f32", pts, c, fk)
     x, y, z = (np64(p) for p in pts)
-    assert oracle.rel_l2(g1, oracle.type1(x, y, z, np64(c), N, eps)) <= 1e-4
-    assert oracle.rel_l2(g2, oracle.type2(x, y, z, np64(fk), eps)) <= 1e-4
+    assert err(g1, oracle.type1(x, y, z, np64(c), N, eps)) <= 1e-4
+    assert err(g2, oracle.type2(x, y, z, np64(fk), eps)) <= 1e-4
 
 
 def test_stage_spread_and_interp_match_oracle(nb):
@@ -118,11 +119,11 @@ def test_stage_spread_and_interp_match_oracle(nb):
     nf = (32, 48, 64)
     g = np64(plan.spread(dev(c)))
     og = oracle.spread(x, y, z, np64(c), nf, w, beta, TWO_PI)
-    assert oracle.rel_l2(g, og) <= 1e-12
+    assert err(g, og) <= 1e-12
     rng = np.random.default_rng(1)
     grid = rng.standard_normal(og.shape) + 1j * rng.standard_normal(og.shape)
     gi = np64(plan.interp(dev(torch.from_numpy(grid))))
-    assert oracle.rel_l2(gi, oracle.interp(x, y, z, grid, w, beta, TWO_PI)) <= 1e-12
+    assert err(gi, oracle.interp(x, y, z, grid, w, beta, TWO_PI)) <= 1e-12
 
 
 @pytest.mark.parametrize("prec", ["f64", "f32"])
@@ -146,9 +147,9 @@ def test_interp_tensor_map_follows_the_grid_address(nb, prec):
     refs = [oracle.interp(x, y, z, g, w, beta, TWO_PI) for g in grids]
     dgrids = [dev(torch.from_numpy(g).to(cdt)) for g in grids]
     for _ in range(2):
-        assert oracle.rel_l2(np64(plan.type2(dev(fk))), o2) <= TOL[prec]
+        assert err(np64(plan.type2(dev(fk))), o2) <= TOL[prec]
         for dg, ref in zip(dgrids, refs):
-            assert oracle.rel_l2(np64(plan.interp(dg)), ref) <= (1e-12 if prec == "f64" else 1e-5)
+            assert err(np64(plan.interp(dg)), ref) <= (1e-12 if prec == "f64" else 1e-5)
 
 
 def test_stage_calls_never_write_past_the_callers_grid(nb):
@@ -180,8 +181,8 @@ def test_nonuniform_shape_signs_modeord_landau(nb):
     x, y, z = (np64(p) for p in pts)
     for iflag in (-1, 1):
         plan, g1, g2 = run_pair(nb, N, eps, "f64", pts, c, fk, L=L, iflag=iflag)
-        assert oracle.rel_l2(g1, oracle.type1(x, y, z, np64(c), N, eps, iflag=iflag, L=L)) <= 1e-10
-        assert oracle.rel_l2(g2, oracle.type2(x, y, z, np64(fk), eps, iflag=iflag, L=L)) <= 1e-10
+        assert err(g1, oracle.type1(x, y, z, np64(c), N, eps, iflag=iflag, L=L)) <= 1e-10
+        assert err(g2, oracle.type2(x, y, z, np64(fk), eps, iflag=iflag, L=L)) <= 1e-10
     # FFT-ordered modes are the centered ones rolled by N/2 per axis
     plan, g1f, _ = run_pair(nb, N, eps, "f64", pts, c, fk, L=L, modeord=1)
     _, g1c, _ = run_pair(nb, N, eps, "f64", pts, c, fk, L=L, modeord=0)
@@ -205,8 +206,8 @@ def test_every_spread_kernel(nb, prec, kernel, eps):
     fk = synthetic.modes(*N).to(c.dtype)
     plan, g1, g2 = run_pair(nb, N, eps, prec, pts, c, fk, tile=tile, spread_warps=kernel)
     x, y, z = (np64(p) for p in pts)
-    assert oracle.rel_l2(g1, oracle.type1(x, y, z, np64(c), N, eps)) <= TOL[prec]
-    assert oracle.rel_l2(g2, oracle.type2(x, y, z, np64(fk), eps)) <= TOL[prec]
+    assert err(g1, oracle.type1(x, y, z, np64(c), N, eps)) <= TOL[prec]
+    assert err(g2, oracle.type2(x, y, z, np64(fk), eps)) <= TOL[prec]
 
 
 @pytest.mark.parametrize("prec", ["f64", "f32"])
@@ -224,8 +225,8 @@ def test_precomputed_weights_both_paths(nb, prec, kernel, precompute):
                             precompute=precompute)
     assert plan.info()["weights_precomputed"] == (1 if precompute == 1 else 0)
     x, y, z = (np64(p) for p in pts)
-    assert oracle.rel_l2(g1, oracle.type1(x, y, z, np64(c), N, eps)) <= TOL[prec]
-    assert oracle.rel_l2(g2, oracle.type2(x, y, z, np64(fk), eps)) <= TOL[prec]
+    assert err(g1, oracle.type1(x, y, z, np64(c), N, eps)) <= TOL[prec]
+    assert err(g2, oracle.type2(x, y, z, np64(fk), eps)) <= TOL[prec]
 
 
 @pytest.mark.parametrize("prec", ["f64", "f32"])
@@ -247,14 +248,14 @@ def test_ablation_variants_atomic_spread_direct_interp(nb, prec, variant, precom
     plan, g1, g2 = run_pair(nb, N, eps, prec, pts, c, fk, spread_warps=sw, interp_method=im,
                             precompute=precompute)
     xs, ys, zs = (np64(p) for p in pts)
-    assert oracle.rel_l2(g1, oracle.type1(xs, ys, zs, np64(c), N, eps)) <= TOL[prec]
-    assert oracle.rel_l2(g2, oracle.type2(xs, ys, zs, np64(fk), eps)) <= TOL[prec]
+    assert err(g1, oracle.type1(xs, ys, zs, np64(c), N, eps)) <= TOL[prec]
+    assert err(g2, oracle.type2(xs, ys, zs, np64(fk), eps)) <= TOL[prec]
     # a second setpts (other points, fewer of them) refreshes the caller-order map
     pts2, c2 = host_inputs(Np // 3, prec, seed=14)
     plan.setpts(*(p.cuda() for p in pts2))
     f = np64(plan.type2(fk.cuda()))
     xs, ys, zs = (np64(p) for p in pts2)
-    assert oracle.rel_l2(f, oracle.type2(xs, ys, zs, np64(fk), eps)) <= TOL[prec]
+    assert err(f, oracle.type2(xs, ys, zs, np64(fk), eps)) <= TOL[prec]
 
 
 def test_custom_and_ragged_tiles(nb):
@@ -267,8 +268,8 @@ def test_custom_and_ragged_tiles(nb):
     for tile in [(4, 4, 4), (7, 9, 5), (16, 8, 4), (32, 12, 3)]:
         plan, g1, g2 = run_pair(nb, N, eps, "f64", pts, c, fk, tile=tile)
         assert tuple(plan.info()["tile"]) == tile
-        assert oracle.rel_l2(g1, o1) <= 1e-10, tile
-        assert oracle.rel_l2(g2, o2) <= 1e-10, tile
+        assert err(g1, o1) <= 1e-10, tile
+        assert err(g2, o2) <= 1e-10, tile
     # a subgrid that cannot fit in one CTA's shared memory is refused at plan time
     with pytest.raises(nb.NufftError):
         nb.Plan(N, eps, tile=(64, 64, 64))
@@ -300,8 +301,8 @@ def test_edge_cases(nb):
         plan.setpts(*(dev(torch.from_numpy(p)) for p in pts))
         g1 = np64(plan.type1(dev(torch.from_numpy(c))))
         g2 = np64(plan.type2(dev(fk)))
-        assert oracle.rel_l2(g1, oracle.type1(*pts, c, N, w_eps, L=L)) <= 1e-10
-        assert oracle.rel_l2(g2, oracle.type2(*pts, np64(fk), w_eps, L=L)) <= 1e-10
+        assert err(g1, oracle.type1(*pts, c, N, w_eps, L=L)) <= 1e-10
+        assert err(g2, oracle.type2(*pts, np64(fk), w_eps, L=L)) <= 1e-10
 
 
 @pytest.mark.parametrize("kernel", [0, 1, 2, 8])
@@ -314,14 +315,14 @@ def test_clustered_points_one_hot_bin(nb, kernel):
     fk = synthetic.modes(*N)
     x, y, z = (np64(p) for p in pts)
     _, g1, g2 = run_pair(nb, N, eps, "f64", pts, c, fk, tile=tile, spread_warps=kernel)
-    assert oracle.rel_l2(g1, oracle.type1(x, y, z, np64(c), N, eps)) <= 1e-10
-    assert oracle.rel_l2(g2, oracle.type2(x, y, z, np64(fk), eps)) <= 1e-10
+    assert err(g1, oracle.type1(x, y, z, np64(c), N, eps)) <= 1e-10
+    assert err(g2, oracle.type2(x, y, z, np64(fk), eps)) <= 1e-10
     one = tuple(torch.full((5000,), 1.2345, dtype=torch.float64) for _ in range(3))
     c1 = synthetic.strengths(5000)
     _, g1, g2 = run_pair(nb, N, eps, "f64", one, c1, fk, tile=tile, spread_warps=kernel)
     o = [np64(p) for p in one]
-    assert oracle.rel_l2(g1, oracle.type1(*o, np64(c1), N, eps)) <= 1e-10
-    assert oracle.rel_l2(g2, oracle.type2(*o, np64(fk), eps)) <= 1e-10
+    assert err(g1, oracle.type1(*o, np64(c1), N, eps)) <= 1e-10
+    assert err(g2, oracle.type2(*o, np64(fk), eps)) <= 1e-10
 
 
 def test_adjointness_fp64(nb):
@@ -346,8 +347,8 @@ def test_host_buffers_through_the_abi(nb):
     h2 = plan.type2(fk.pin_memory())
     assert not h1.is_cuda and not h2.is_cuda
     _, g1, g2 = run_pair(nb, N, eps, "f64", pts, c, fk)
-    assert oracle.rel_l2(np64(h1), g1) <= 1e-13
-    assert oracle.rel_l2(np64(h2), g2) <= 1e-13
+    assert err(np64(h1), g1) <= 1e-13
+    assert err(np64(h2), g2) <= 1e-13
 
 
 def test_config2_fp32_full_parity(nb):
@@ -358,9 +359,9 @@ def test_config2_fp32_full_parity(nb):
     x, y, z = (np64(p) for p in pts)
     for eps in (1e-4, 1e-6):
         _, g1, g2 = run_pair(nb, N, eps, "f32", pts, c, fk)
-        assert oracle.rel_l2(g1, oracle.type1(x, y, z, np64(c), N, eps)) <= 1e-4
-        assert oracle.rel_l2(g2, oracle.type2(x, y, z, np64(fk), eps)) <= 1e-4
+        assert err(g1, oracle.type1(x, y, z, np64(c), N, eps)) <= 1e-4
+        assert err(g2, oracle.type2(x, y, z, np64(fk), eps)) <= 1e-4
         rng = np.random.default_rng(3)
         sm = rng.choice(np.prod(N), 300, replace=False)
-        e1 = oracle.rel_l2(g1.ravel()[sm], oracle.nudft1(x, y, z, np64(c), N, sel=sm))
+        e1 = err(g1.ravel()[sm], oracle.nudft1(x, y, z, np64(c), N, sel=sm))
         assert e1 <= 10 * eps
