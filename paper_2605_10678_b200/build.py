@@ -30,7 +30,7 @@ CU_FLAGS = ARCH + COMMON + ["--expt-relaxed-constexpr", "-Xptxas", "-v"]
 # developer instrumentation only (e.g. -DNUFFT_OUTER_PROF); never set for the product build
 CU_FLAGS += os.environ.get("NUFFT_EXTRA_NVCC_FLAGS", "").split()
 
-SOURCES = ["sort.cu", "spread.cu", "spread_rows.cu", "spread_outer.cu", "interp.cu",
+SOURCES = ["sort.cu", "spread.cu", "spread_rows.cu", "spread_outer.cu", "spread_sub.cu", "interp.cu", "interp_real.cu", "interp_vec3.cu",
            "elementwise.cu", "pif.cu", "variants.cu", "spread_tc.cu", "dist_kernels.cu", "peak.cu", "plan.cpp", "dist.cpp"]
 
 
@@ -46,10 +46,35 @@ def _nccl_dirs():
     return None, None
 
 
+def _includes(path):
+    """Local headers #include-d by `path` (quoted includes resolved in csrc/ or include/)."""
+    out = []
+    try:
+        with open(path) as f:
+            for line in f:
+                line = line.strip()
+                if line.startswith("#include \""):
+                    name = line.split('"')[1]
+                    for d in (os.path.dirname(path), CSRC, os.path.join(ROOT, "include")):
+                        cand = os.path.normpath(os.path.join(d, name))
+                        if os.path.exists(cand):
+                            out.append(cand)
+                            break
+    except OSError:
+        pass
+    return out
+
+
 def _deps(src):
-    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
-    headers.append(os.path.join(ROOT, "include", "nufft.h"))
-    return [os.path.join(CSRC, src)] + headers
+    """The source and every local header it includes, transitively."""
+    seen, todo = [], [os.path.join(CSRC, src)]
+    while todo:
+        f = todo.pop()
+        if f in seen:
+            continue
+        seen.append(f)
+        todo.extend(_includes(f))
+    return seen
 
 
 def _stale(target, deps):

@@ -36,6 +36,13 @@ struct Geom {
     // exist (ghost halos accumulated / filled over NCCL)
     int zper;
     int hz_lo, hz_hi;
+    // sub-bins (spread_warps = 5): every bin is split into ns[0] x ns[1] x ns[2]
+    // cubes of G stencil-base values per axis (G = 9 - w: a sub-bin's stencils span
+    // 8 cells per axis); setpts sorts by (bin, sub-bin) and keeps the sub-bin
+    // offsets.  nsub = 1, G = 0: no sub-bins
+    int G;
+    int ns[3];
+    int nsub;
 };
 
 // Local z row of a subgrid: periodic wrap on one GPU; on a slab, -1e9 marks a
@@ -64,6 +71,7 @@ static_assert(sizeof(PtRec<double>) == 32 && sizeof(PtRec<float>) == 32, "one se
 
 template <typename T> struct PtsView {
     const uint32_t* offset;  // nbins + 1 bin starts (exclusive scan of counts)
+    const uint32_t* offset_sub;  // nbins nsub + 1 sub-bin starts (Geom::nsub > 1), else = offset
     const PtRec<T>* rec;     // Np sorted records
     const T* w;              // Np x 3w ES weights in sorted order ([x | y | z] per point,
                              // node k of axis d at 3w i + w d + k), or nullptr: evaluate phi
@@ -71,11 +79,13 @@ template <typename T> struct PtsView {
 
 // ---------------------------------------------------------------- kernel launchers
 // sort.cu
+// sort keys = nbins nsub (bin-major, sub-bin minor); offset_key: nkeys + 1 starts;
+// offset (nbins + 1 bin starts) is gathered from it when nsub > 1 (else the same array)
 template <typename T>
 cudaError_t launch_bin_sort(const Geom& g, int64_t Np, const T* x, const T* y, const T* z,
-                            uint32_t* count, uint32_t* offset, uint32_t* blocksum,
-                            uint32_t* bin_of, uint32_t* rank_of, PtRec<T>* rec, int64_t nbins,
-                            cudaStream_t s);
+                            uint32_t* count, uint32_t* offset_key, uint32_t* offset,
+                            uint32_t* blocksum, uint32_t* bin_of, uint32_t* rank_of,
+                            PtRec<T>* rec, int64_t nbins, cudaStream_t s);
 size_t scan_blocksum_elems(int64_t nbins);
 // setpts (precompute): w[3w i + w d + k] = phi(2 (k - rec[i].d[d]) / w)
 template <typename T>
@@ -114,7 +124,7 @@ template <typename T>
 cudaError_t launch_caller_order(const PtRec<T>* rec, int64_t Np, uint32_t* order,
                                 cudaStream_t s);
 // smem row pitch (cells) of the interp's subgrid for complex cells of cell_bytes
-int interp_tile_pitch(int cell_bytes, int T, int W);
+int interp_tile_pitch(int cell_bytes, int T, int W, bool sub = false);
 template <typename T>
 cudaError_t launch_spread_real(const Geom& g, const PtsView<T>& p, int64_t nbins, const T* c,
                                T* grid, double beta, cudaStream_t s);
@@ -137,6 +147,16 @@ cudaError_t launch_spread_rows(const Geom& g, const PtsView<T>& p, int64_t nbins
                                const typename Cx<T>::type* c, typename Cx<T>::type* grid,
                                double beta, cudaStream_t s);
 template <typename T> size_t spread_rows_smem_bytes(const Geom& g);
+// spread_sub.cu: sub-bin register-row spread (Geom::nsub > 1, w <= 6)
+bool spread_sub_applies(const Geom& g);
+template <typename T>
+cudaError_t launch_spread_sub(const Geom& g, const PtsView<T>& p, int64_t nbins,
+                              const typename Cx<T>::type* c, typename Cx<T>::type* grid,
+                              double beta, cudaStream_t s);
+template <typename T>
+cudaError_t launch_spread_sub_real(const Geom& g, const PtsView<T>& p, int64_t nbins, const T* c,
+                                   T* grid, double beta, cudaStream_t s);
+template <typename T> size_t spread_sub_smem_bytes(const Geom& g);
 // spread_outer.cu: per-plane outer-product spread (w <= 12 and T = 16 - w on every axis)
 bool spread_outer_applies(const Geom& g);
 template <typename T>

@@ -1,394 +1,9 @@
-// interp.cu -- the interpolation operator C^T of Eq. (4).
-//
-// "Sorted interpolation" taken to its B200 form: one CTA per
-// bin stages the bin's (T + w)^3 subgrid from the periodic fine grid into
-// shared memory once, with the bulk-async (TMA) engine: one
-// cp.async.bulk.shared::cta.global (SASS UBLKCP) per contiguous row segment,
-// all completing on a single mbarrier transaction count; rows that cross the
-// periodic boundary split into two segments.  Every point of the bin then
-// gathers its w^3 stencil from shared memory, so each grid cell is read from
-// HBM about ((T + w) / T)^3 times per transform instead of w^3 / (points per
-// cell) times as in direct interpolation.
-//
-// Points are handled in chunks of 32 per warp (the bin split evenly over the
-// warps): lane l loads point l's sorted record (coalesced) and evaluates its
-// 3w ES weights in registers (separability; phi direct,
-// PAPER.md:176), parking them in a per-warp shared buffer.  The warp then
-// walks the 32 points: lane slots cover the w x w (x, y) columns of the
-// stencil, each sums its w z-cells against wz, scales by wx*wy, and a shuffle
-// reduction yields c_j, written in the caller's order (c[perm[slot]]).  The
-// kernel is bound by shared-memory wavefronts (one 8- or 16-byte cell load per
-// stencil cell), so the slot map is chosen for them: for w >= 6 a quarter-warp
-// reads 8 consecutive cells of ONE row (x = lane % 8, y = lane / 8 + 4 pass),
-// conflict-free for any row pitch; for w <= 5 the flat map over the w^2 columns
-// wastes fewer lanes.
-#include <cuda.h>
-
-#include <cstring>
-#include <type_traits>
-
-#include "device_util.cuh"
-#include "internal.cuh"
+// interp.cu -- C^T for complex grids, plus the plan-level helpers.
+// Kernels and launch templates: interp_impl.cuh (one translation unit per value
+// type so the template instances compile in parallel).
+#include "interp_impl.cuh"
 
 namespace nufft {
-
-namespace {
-
-using namespace dev;
-
-constexpr int kInterpThreads = 256;
-constexpr int kInterpWarps = kInterpThreads / 32;
-
-// V: value type of the grid and of the outputs, Cx<T> (complex) or T (real)
-template <typename T, typename V, int W>
-struct InterpSmem {
-    using C = V;
-    // per-point weight stride in elements, ODD: lane l stores its point's weights
-    // at l * WS, so the 32 (fp32) / 16 (fp64 half-warp) lanes of a store hit
-    // distinct banks (an even stride such as 16 at w = 5 serialises them 16-32 way)
-    static constexpr int WS = (3 * W + 1) | 1;
-    static size_t bytes(int ncell) {
-        return (size_t)ncell * sizeof(C) + (size_t)kInterpWarps * 32 * WS * sizeof(T) + 16;
-    }
-};
-
-// Grid values with NC real components: complex (2), real (1), or a real 3-vector
-// (3: the three field components of the PIF gather, sharing one weight evaluation).
-template <typename T> struct Vec3 { T c[3]; };
-template <typename V> struct VT;
-template <> struct VT<float2> {
-    static constexpr int n = 2;
-    __device__ static float get(const float2& v, int k) { return k ? v.y : v.x; }
-    __device__ static float2 make(const float (&a)[2]) { return float2{a[0], a[1]}; }
-};
-template <> struct VT<double2> {
-    static constexpr int n = 2;
-    __device__ static double get(const double2& v, int k) { return k ? v.y : v.x; }
-    __device__ static double2 make(const double (&a)[2]) { return double2{a[0], a[1]}; }
-};
-template <> struct VT<float> {
-    static constexpr int n = 1;
-    __device__ static float get(const float& v, int) { return v; }
-    __device__ static float make(const float (&a)[1]) { return a[0]; }
-};
-template <> struct VT<double> {
-    static constexpr int n = 1;
-    __device__ static double get(const double& v, int) { return v; }
-    __device__ static double make(const double (&a)[1]) { return a[0]; }
-};
-template <typename T> struct VT<Vec3<T>> {
-    static constexpr int n = 3;
-    __device__ static T get(const Vec3<T>& v, int k) { return v.c[k]; }
-    __device__ static Vec3<T> make(const T (&a)[3]) { return Vec3<T>{{a[0], a[1], a[2]}}; }
-};
-// Grid / shared-memory layout per value type: one tile of V cells, or -- for the
-// 3-vector -- three component grids (SoA, gstride reals apart in HBM) staged into
-// three consecutive component tiles (cell = one real).
-template <typename V> struct Layout {
-    using Cell = V;
-    static constexpr int comps = 1;
-    __device__ static V load(const Cell* t, int o, int) { return t[o]; }
-};
-template <typename T> struct Layout<Vec3<T>> {
-    using Cell = T;
-    static constexpr int comps = 3;
-    __device__ static Vec3<T> load(const T* t, int o, int nc) {
-        return Vec3<T>{{t[o], t[o + nc], t[o + 2 * nc]}};
-    }
-};
-
-// sv[m] = sum_k G[col + k plane].m wz[k] over the w planes of one stencil column;
-// complex fp32 cells take one packed FFMA2 per cell (device_util.cuh vfma)
-template <typename V, int W, typename T, int NC>
-__device__ __forceinline__ void zsum(T (&sv)[NC], const typename Layout<V>::Cell* tile, int col,
-                                     int plane, int ncell, const T (&wz)[W]) {
-    if constexpr (std::is_same<V, float2>::value) {
-        float2 a = float2{0.0f, 0.0f};
-#pragma unroll
-        for (int k = 0; k < W; ++k) vfma(a, tile[col + k * plane], wz[k]);
-        sv[0] = a.x;
-        sv[1] = a.y;
-    } else {
-#pragma unroll
-        for (int m = 0; m < NC; ++m) sv[m] = 0;
-#pragma unroll
-        for (int k = 0; k < W; ++k) {
-            const V v = Layout<V>::load(tile, col + k * plane, ncell);
-#pragma unroll
-            for (int m = 0; m < NC; ++m) sv[m] += VT<V>::get(v, m) * wz[k];
-        }
-    }
-}
-
-// Output stage of the gather: store the value at the caller's index ...
-template <typename V> struct StoreOut {
-    V* out;
-    template <typename T, int NC>
-    __device__ void operator()(uint32_t pj, const T (&tot)[NC]) const { out[pj] = VT<V>::make(tot); }
-};
-// ... or, for the PIF field gather, fuse the leapfrog kick:
-// v_d[pj] += s E_d(x_pj) for the three components (no field array in HBM)
-template <typename T> struct KickOut {
-    T* v0;
-    T* v1;
-    T* v2;
-    T s;
-    template <int NC>
-    __device__ void operator()(uint32_t pj, const T (&tot)[NC]) const {
-        static_assert(NC == 3, "a 3-component gather");
-        v0[pj] += s * tot[0];
-        v1[pj] += s * tot[1];
-        v2[pj] += s * tot[2];
-    }
-};
-
-// Four per-lane partial sums (points j0 .. j0 + 3) -> the total of point
-// j0 + (lane & 16 ? 1 : 0) + (lane & 8 ? 2 : 0) on every lane: a transposing
-// butterfly (offsets 16, 8 split the 4 sums over lane octets, 4, 2, 1 finish).
-template <typename T>
-__device__ __forceinline__ T reduce4(const T (&v)[4], int lane) {
-    const bool h16 = lane & 16, h8 = lane & 8;
-    T r0 = h16 ? v[1] : v[0], r1 = h16 ? v[3] : v[2];
-    r0 += __shfl_xor_sync(0xffffffffu, h16 ? v[0] : v[1], 16);
-    r1 += __shfl_xor_sync(0xffffffffu, h16 ? v[2] : v[3], 16);
-    T rr = h8 ? r1 : r0;
-    rr += __shfl_xor_sync(0xffffffffu, h8 ? r0 : r1, 8);
-#pragma unroll
-    for (int o = 4; o > 0; o >>= 1) rr += __shfl_xor_sync(0xffffffffu, rr, o);
-    return rr;
-}
-
-template <typename T, typename V, int W, typename Out>
-__global__ void __launch_bounds__(kInterpThreads, 2)
-    interp_tile_kernel(Geom g, PtsView<T> p, const typename Layout<V>::Cell* __restrict__ grid,
-                       int64_t gstride, Out out, T beta, const __grid_constant__ CUtensorMap tmap,
-                       int use_tmap) {
-    using C = V;
-    using Cell = typename Layout<V>::Cell;
-    constexpr int NCOMP = Layout<V>::comps;  // component tiles (3 for the SoA 3-vector)
-    constexpr int NC = VT<V>::n;  // real components per value
-    constexpr bool kFlat = W <= 5;
-    constexpr int NQ = kFlat ? (W * W + 31) / 32 : 1;
-    constexpr int XS = W <= 8 ? 8 : 16, YS = 32 / XS, NPASS = (W + YS - 1) / YS;
-    constexpr int WS = InterpSmem<T, V, W>::WS;
-    constexpr int NW = kInterpWarps;
-    extern __shared__ __align__(1024) unsigned char smem[];  // TMA tensor destination
-
-    const int b = blockIdx.x;
-    const uint32_t beg = p.offset[b], end = p.offset[b + 1];
-    if (beg == end) return;
-
-    const int bx = b % g.nb[0], by = (b / g.nb[0]) % g.nb[1], bz = b / (g.nb[0] * g.nb[1]);
-    const TileX tx = tile_x<sizeof(Cell)>(bx, g.T[0], W);
-    const int Ey = g.T[1] + W, Ez = g.T[2] + W;
-    const int pitch = tx.pitch, plane = pitch * Ey, ncell = plane * Ez;
-    Cell* tile = reinterpret_cast<Cell*>(smem);  // NCOMP tiles of ncell cells
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    T* wb = reinterpret_cast<T*>(tile + NCOMP * ncell) + warp * 32 * WS;  // [32][WS] per warp
-    uint64_t* bar = reinterpret_cast<uint64_t*>(
-        (reinterpret_cast<uintptr_t>(reinterpret_cast<T*>(tile + NCOMP * ncell) + NW * 32 * WS) + 15) &
-        ~(uintptr_t)15);
-
-    // ---- stage the subgrid (one mbarrier transaction).  A bin whose subgrid lies
-    // inside the grid (no periodic wrap) is ONE 3D TMA tensor copy of the whole box;
-    // the others take one bulk copy per row segment, split at the periodic boundary.
-    const int oy0 = by * g.T[1] - W / 2, oz0 = bz * g.T[2] - W / 2;
-    const bool interior = use_tmap && tx.gx0 >= 0 && tx.gx0 + tx.len <= (int)g.nf[0] &&
-                          oy0 >= 0 && oy0 + Ey <= (int)g.nf[1] && oz0 >= 0 &&
-                          oz0 + Ez <= (int)g.nz_loc;
-    if (threadIdx.x == 0) {
-        mbar_init(bar, 1);
-        mbar_arrive_expect_tx(bar, interior ? (unsigned)(Ez * Ey * pitch * sizeof(Cell))
-                                            : (unsigned)(NCOMP * Ey * Ez * tx.len * sizeof(Cell)));
-    }
-    __syncthreads();
-    if (interior) {
-        if (threadIdx.x == 0) {
-            constexpr int R = (int)(sizeof(Cell) / sizeof(T));  // map elements per cell
-            asm volatile(
-                "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-                " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_addr(tile)),
-                "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(tx.gx0 * R), "r"(oy0), "r"(oz0),
-                "r"(smem_addr(bar))
-                : "memory");
-        }
-    } else {
-        const int oy = by * g.T[1] - W / 2, oz = bz * g.T[2] - W / 2;
-        const int nfx = (int)g.nf[0], nfy = (int)g.nf[1];
-        int sg[2], ss[2], sn[2];
-        const int nseg = row_segments(tx.gx0, tx.len, nfx, sg, ss, sn);
-        for (int r = threadIdx.x; r < Ey * Ez; r += kInterpThreads) {
-            const int cz = r / Ey, cy = r - cz * Ey;
-            int gz = z_row(oz + cz, g);
-            // a row beyond the halo-extended slab is read by no stencil: stage any
-            // valid row there (the transaction count stays one full subgrid)
-            if (gz < -g.hz_lo) gz = 0;
-            const int gy = wrap1(oy + cy, nfy);
-#pragma unroll
-            for (int cc = 0; cc < NCOMP; ++cc) {
-                const Cell* grow = grid + cc * gstride + (int64_t)nfx * ((int64_t)gz * nfy + gy);
-                Cell* trow = tile + cc * ncell + r * pitch;
-                for (int k = 0; k < nseg; ++k)
-                    bulk_g2s(trow + ss[k], grow + sg[k], (unsigned)(sn[k] * sizeof(Cell)), bar);
-            }
-        }
-    }
-
-    // lane slots.  w <= 5: flat slots s = lane + 32 q over the w x w columns
-    // (x = s % w, y = s / w); w >= 6: x = lane % XS, y = lane / XS + YS * pass
-    // (one 8-cell row per 128-bit quarter-warp phase: no bank conflicts)
-    const int sx = lane % XS, sy0 = lane / XS;
-    int qoff[NQ], qx[NQ], qy[NQ];
-    bool qok[NQ];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-        const int s = lane + 32 * q;
-        qok[q] = s < W * W;
-        qx[q] = qok[q] ? s % W : 0;
-        qy[q] = qok[q] ? s / W : 0;
-        qoff[q] = qy[q] * pitch + qx[q];
-    }
-    const T two_over_w = (T)2 / (T)W;
-    const uint32_t n = end - beg;
-    const uint32_t wbeg = beg + (uint32_t)(((uint64_t)n * warp) / NW);
-    const uint32_t wend = beg + (uint32_t)(((uint64_t)n * (warp + 1)) / NW);
-    bool staged = false;
-
-    for (uint32_t c0 = wbeg; c0 < wend; c0 += 32) {
-        // ---- lane l: record + 3w weights of point c0 + l (overlaps the tile load)
-        const uint32_t slot = c0 + lane;
-        uint32_t my_perm = 0;
-        int my_base = 0;
-        if (slot < wend) {
-            const PtRec<T> rr = p.rec[slot];
-            const T d3[3] = {rr.d[0], rr.d[1], rr.d[2]};
-            const uint32_t la = rr.la;
-            my_perm = rr.perm;
-            my_base = (int)(((la >> 16) * Ey + ((la >> 8) & 0xff)) * pitch + (la & 0xff)) +
-                      tx.shift;
-            if (!p.w) {
-                T* wl = wb + lane * WS;
-#pragma unroll
-                for (int d = 0; d < 3; ++d)
-#pragma unroll
-                    for (int k = 0; k < W; ++k)
-                        wl[d * W + k] = es_weight<T>(((T)k - d3[d]) * two_over_w, beta);
-            }
-        }
-        if (p.w) {  // precomputed at setpts: the chunk's rows are contiguous, copy coalesced
-            const T* src = p.w + (size_t)c0 * (3 * W);
-            const int ne = (int)min(32u, wend - c0) * (3 * W);
-            for (int e = lane; e < ne; e += 32) {
-                const int j = e / (3 * W);
-                wb[j * WS + (e - j * (3 * W))] = src[e];
-            }
-        }
-        if (!staged) {
-            mbar_wait(bar, 0);
-            staged = true;
-        }
-        __syncwarp();
-        const int np = (int)min(32u, wend - c0);
-        // four points at a time: independent accumulations, then a transposing
-        // butterfly (offsets 16, 8 split the 4 sums over lane octets, 4, 2, 1 finish)
-        for (int j0 = 0; j0 < np; j0 += 4) {
-            T acc[NC][4];
-#pragma unroll
-            for (int g4 = 0; g4 < 4; ++g4) {
-                const int j = j0 + g4;
-#pragma unroll
-                for (int q = 0; q < NC; ++q) acc[q][g4] = 0;
-                if (j < np) {
-                    const int base = __shfl_sync(0xffffffffu, my_base, j);
-                    const T* wj = wb + j * WS;
-                    T wz[W];
-#pragma unroll
-                    for (int k = 0; k < W; ++k) wz[k] = wj[2 * W + k];
-                    if constexpr (kFlat) {
-#pragma unroll
-                        for (int q = 0; q < NQ; ++q) {
-                            if (qok[q]) {
-                                const int col = base + qoff[q];
-                                T sv[NC];
-                                zsum<C, W>(sv, tile, col, plane, ncell, wz);
-                                const T wxy = wj[qx[q]] * wj[W + qy[q]];
-#pragma unroll
-                                for (int m = 0; m < NC; ++m) acc[m][g4] += sv[m] * wxy;
-                            }
-                        }
-                    } else {
-                        const int col0 = base + sx;
-#pragma unroll
-                        for (int ps = 0; ps < NPASS; ++ps) {
-                            const int y = sy0 + YS * ps;
-                            if (sx < W && y < W) {
-                                const int col = col0 + y * pitch;
-                                T sv[NC];
-                                zsum<C, W>(sv, tile, col, plane, ncell, wz);
-                                const T wy = wj[W + y];
-#pragma unroll
-                                for (int m = 0; m < NC; ++m) acc[m][g4] += sv[m] * wy;
-                            }
-                        }
-                        const T wx = sx < W ? wj[sx] : (T)0;
-#pragma unroll
-                        for (int m = 0; m < NC; ++m) acc[m][g4] *= wx;
-                    }
-                }
-            }
-            T tot[NC];
-#pragma unroll
-            for (int m = 0; m < NC; ++m) tot[m] = reduce4<T>(acc[m], lane);
-            const int j = j0 + ((lane & 16) ? 1 : 0) + ((lane & 8) ? 2 : 0);
-            const uint32_t pj = __shfl_sync(0xffffffffu, my_perm, j & 31);
-            if ((lane & 7) == 0 && j < np) out(pj, tot);
-        }
-        __syncwarp();
-    }
-    // a warp without points must not exit before the bulk copies into this CTA's
-    // shared memory have landed
-    if (!staged) mbar_wait(bar, 0);
-}
-
-template <typename T, typename V, int W>
-size_t smem_w(const Geom& g) {
-    using Cell = typename Layout<V>::Cell;
-    return InterpSmem<T, V, W>::bytes(tile_pitch<sizeof(Cell)>(g.T[0], W) * (g.T[1] + W) *
-                                      (g.T[2] + W));
-}
-
-template <typename T, typename V, int W, typename Out = StoreOut<V>>
-cudaError_t launch_w(const Geom& g, const PtsView<T>& p, int64_t nbins,
-                     const typename Layout<V>::Cell* grid, Out c, double beta, cudaStream_t s,
-                     int64_t gstride = 0, const void* tmap = nullptr) {
-    const size_t smem = smem_w<T, V, W>(g);
-    auto kern = interp_tile_kernel<T, V, W, Out>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        return e;
-    }
-    CUtensorMap map;
-    std::memset(&map, 0, sizeof(map));
-    if (tmap) std::memcpy(&map, tmap, sizeof(map));
-    if (nbins > 0)
-        kern<<<(unsigned)nbins, kInterpThreads, smem, s>>>(g, p, grid, gstride, c, (T)beta, map,
-                                                           tmap ? 1 : 0);
-    return cudaGetLastError();
-}
-
-}  // namespace
-
-#define NUFFT_W_SWITCH(CALL)                                                              \
-    switch (g.w) {                                                                        \
-        case 2: return CALL(2); case 3: return CALL(3); case 4: return CALL(4);          \
-        case 5: return CALL(5); case 6: return CALL(6); case 7: return CALL(7);          \
-        case 8: return CALL(8); case 9: return CALL(9); case 10: return CALL(10);        \
-        case 11: return CALL(11); case 12: return CALL(12); case 13: return CALL(13);    \
-        case 14: return CALL(14); case 15: return CALL(15); case 16: return CALL(16);    \
-        default: break;                                                                   \
-    }
 
 template <typename T>
 cudaError_t launch_interp(const Geom& g, const PtsView<T>& p, int64_t nbins,
@@ -403,41 +18,6 @@ cudaError_t launch_interp(const Geom& g, const PtsView<T>& p, int64_t nbins,
 }
 
 template <typename T>
-cudaError_t launch_interp_real(const Geom& g, const PtsView<T>& p, int64_t nbins, const T* grid,
-                               T* c, double beta, cudaStream_t s) {
-#define CALL(WW) launch_w<T, T, WW>(g, p, nbins, grid, StoreOut<T>{c}, beta, s)
-    NUFFT_W_SWITCH(CALL)
-#undef CALL
-    return cudaErrorInvalidValue;
-}
-
-// grid = three real grids nf1 nf2 nz (x fastest), gstride reals apart; out = Np
-// 3-vectors of reals (caller order)
-template <typename T>
-cudaError_t launch_interp_vec3(const Geom& g, const PtsView<T>& p, int64_t nbins, const T* grid,
-                               int64_t gstride, T* c, double beta, cudaStream_t s) {
-#define CALL(WW)                                                                          \
-    launch_w<T, Vec3<T>, WW>(g, p, nbins, grid,                                           \
-                             StoreOut<Vec3<T>>{reinterpret_cast<Vec3<T>*>(c)}, beta, s, gstride)
-    NUFFT_W_SWITCH(CALL)
-#undef CALL
-    return cudaErrorInvalidValue;
-}
-
-// the same gather with the PIF kick fused into its output: v_d += s E_d
-template <typename T>
-cudaError_t launch_interp_vec3_kick(const Geom& g, const PtsView<T>& p, int64_t nbins,
-                                    const T* grid, int64_t gstride, T* v0, T* v1, T* v2,
-                                    double scale, double beta, cudaStream_t s) {
-#define CALL(WW)                                                                          \
-    launch_w<T, Vec3<T>, WW>(g, p, nbins, grid, KickOut<T>{v0, v1, v2, (T)scale}, beta, s,   \
-                             gstride)
-    NUFFT_W_SWITCH(CALL)
-#undef CALL
-    return cudaErrorInvalidValue;
-}
-
-template <typename T>
 size_t interp_smem_bytes(const Geom& g) {
 #define CALL(WW) smem_w<T, typename Cx<T>::type, WW>(g)
     NUFFT_W_SWITCH(CALL)
@@ -445,9 +25,11 @@ size_t interp_smem_bytes(const Geom& g) {
     return 0;
 }
 
-int interp_tile_pitch(int cell_bytes, int T, int W) {
+int interp_tile_pitch(int cell_bytes, int T, int W, bool sub) {
+    if (sub) return cell_bytes == 16 ? sub_pitch<16>(tile_len<16>(T, W)) : sub_pitch<8>(tile_len<8>(T, W));
     return cell_bytes == 16 ? tile_pitch<16>(T, W) : tile_pitch<8>(T, W);
 }
+
 
 template cudaError_t launch_interp<float>(const Geom&, const PtsView<float>&, int64_t,
                                           const float2*, float2*, double, cudaStream_t,
@@ -455,21 +37,6 @@ template cudaError_t launch_interp<float>(const Geom&, const PtsView<float>&, in
 template cudaError_t launch_interp<double>(const Geom&, const PtsView<double>&, int64_t,
                                            const double2*, double2*, double, cudaStream_t,
                                            const void*);
-template cudaError_t launch_interp_real<float>(const Geom&, const PtsView<float>&, int64_t,
-                                               const float*, float*, double, cudaStream_t);
-template cudaError_t launch_interp_real<double>(const Geom&, const PtsView<double>&, int64_t,
-                                                const double*, double*, double, cudaStream_t);
-template cudaError_t launch_interp_vec3<float>(const Geom&, const PtsView<float>&, int64_t,
-                                               const float*, int64_t, float*, double, cudaStream_t);
-template cudaError_t launch_interp_vec3<double>(const Geom&, const PtsView<double>&, int64_t,
-                                                const double*, int64_t, double*, double,
-                                                cudaStream_t);
-template cudaError_t launch_interp_vec3_kick<float>(const Geom&, const PtsView<float>&, int64_t,
-                                                    const float*, int64_t, float*, float*, float*,
-                                                    double, double, cudaStream_t);
-template cudaError_t launch_interp_vec3_kick<double>(const Geom&, const PtsView<double>&, int64_t,
-                                                     const double*, int64_t, double*, double*,
-                                                     double*, double, double, cudaStream_t);
 template size_t interp_smem_bytes<float>(const Geom&);
 template size_t interp_smem_bytes<double>(const Geom&);
 

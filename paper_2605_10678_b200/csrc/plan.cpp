@@ -168,6 +168,7 @@ template <typename T>
 PtsView<T> pts_view(nufft_plan_s* p) {
     PtsView<T> v;
     v.offset = p->offset;
+    v.offset_sub = p->offset_key ? p->offset_key : p->offset;
     v.rec = static_cast<const PtRec<T>*>(p->rec);
     v.w = p->wts_on ? static_cast<const T*>(p->wts) : nullptr;
     return v;
@@ -214,13 +215,15 @@ int local_sort(nufft_plan_s* p, int64_t Np, const void* xd, const void* yd, cons
     if (p->prec == NUFFT_F64)
         NUFFT_CK(launch_bin_sort<double>(p->geom, Np, static_cast<const double*>(xd),
                                          static_cast<const double*>(yd),
-                                         static_cast<const double*>(zd), p->count, p->offset,
+                                         static_cast<const double*>(zd), p->count,
+                                         p->offset_key ? p->offset_key : p->offset, p->offset,
                                          p->blocksum, bin_of, rank_of,
                                          static_cast<PtRec<double>*>(p->rec), p->nbins, p->stream));
     else
         NUFFT_CK(launch_bin_sort<float>(p->geom, Np, static_cast<const float*>(xd),
                                         static_cast<const float*>(yd),
-                                        static_cast<const float*>(zd), p->count, p->offset,
+                                        static_cast<const float*>(zd), p->count,
+                                         p->offset_key ? p->offset_key : p->offset, p->offset,
                                         p->blocksum, bin_of, rank_of,
                                         static_cast<PtRec<float>*>(p->rec), p->nbins, p->stream));
     p->Np = Np;
@@ -314,6 +317,17 @@ int do_spread(nufft_plan_s* p, const void* c_dev, void* grid0) {
                                   p->beta, p->stream));
         return NUFFT_OK;
     }
+    if (p->geom.spread_warps == 5) {  // sub-bin register rows (plan checked the geometry)
+        if (p->prec == NUFFT_F64)
+            NUFFT_CK(launch_spread_sub<double>(p->geom, pts_view<double>(p), p->nbins,
+                                               static_cast<const double2*>(c_dev),
+                                               static_cast<double2*>(grid0), p->beta, p->stream));
+        else
+            NUFFT_CK(launch_spread_sub<float>(p->geom, pts_view<float>(p), p->nbins,
+                                              static_cast<const float2*>(c_dev),
+                                              static_cast<float2*>(grid0), p->beta, p->stream));
+        return NUFFT_OK;
+    }
     const bool rows = p->geom.spread_warps == 1;  // register-row kernel (plan checked it applies)
     const bool outer = p->geom.spread_warps == 2;  // plane outer-product kernel (ditto)
     if (outer && p->prec == NUFFT_F64)
@@ -350,7 +364,15 @@ int do_spread_real(nufft_plan_s* p, const void* c_dev, void* grid) {
     // no real register-row or ablation kernels: real transforms take the z-plane owners
     if (g.spread_warps == 1 || g.spread_warps < 0) g.spread_warps = 8;
     if (g.spread_warps == 3) g.spread_warps = 2;  // the register outer products
-    if (g.spread_warps == 2 && p->prec == NUFFT_F64)
+    if (g.spread_warps == 5 && p->prec == NUFFT_F64)
+        NUFFT_CK(launch_spread_sub_real<double>(g, pts_view<double>(p), p->nbins,
+                                                static_cast<const double*>(c_dev),
+                                                static_cast<double*>(grid), p->beta, p->stream));
+    else if (g.spread_warps == 5)
+        NUFFT_CK(launch_spread_sub_real<float>(g, pts_view<float>(p), p->nbins,
+                                               static_cast<const float*>(c_dev),
+                                               static_cast<float*>(grid), p->beta, p->stream));
+    else if (g.spread_warps == 2 && p->prec == NUFFT_F64)
         NUFFT_CK(launch_spread_outer_real<double>(g, pts_view<double>(p), p->nbins,
                                                   static_cast<const double*>(c_dev),
                                                   static_cast<double*>(grid), p->beta, p->stream));
@@ -430,7 +452,8 @@ static const void* interp_tmap(nufft_plan_s* p, const void* grid0) {
     if (p->tmap_state < 0 || grid0 == nullptr) return nullptr;
     if (p->tmap_state == 1 && p->tmap_grid == grid0) return p->tmap;
     const int w = p->w, r = (int)p->real_size;
-    const int pitch = interp_tile_pitch(2 * r, p->geom.T[0], w);
+    const int pitch = interp_tile_pitch(2 * r, p->geom.T[0], w,
+                                        p->geom.nsub > 1 && w <= 6);  // the sub-bin gather's rows
     const cuuint64_t dim[3] = {(cuuint64_t)(2 * p->nf[0]), (cuuint64_t)p->nf[1],
                                (cuuint64_t)p->geom.nz_loc};
     const cuuint64_t stride[2] = {(cuuint64_t)(2 * p->nf[0] * r),
@@ -509,6 +532,21 @@ int default_tile(int w, int prec, int64_t nf) {
     return t;
 }
 
+bool spread_sub_width(int w) { return w >= 2 && w <= 6; }
+
+// Sub-bin spread (spread_warps = 5): G = 9 - w stencil bases per sub-bin and axis
+// (the stencils of a sub-bin span 8 cells: the 8 x 8 register rows of a warp), ns
+// sub-bins per bin axis, T = ns G - 1 (la in [0, T] covers ns G values); ns chosen
+// so that the (T + w)^3 subgrid stays <= 20^3 cells
+int sub_default_tile(int w, int64_t nf) {
+    const int G = 9 - w;
+    int ns = 1;
+    while ((ns + 1) * G - 1 + w <= 20) ++ns;
+    int t = ns * G - 1;
+    while (t > 0 && t + w + 2 > nf) t -= G;  // tiny grids
+    return t;
+}
+
 int ensure_complex_fft(nufft_plan_s* p) {
     if (p->fft_ok) return NUFFT_OK;
     if (cufftPlan3d(&p->fft, (int)p->nf[2], (int)p->nf[1], (int)p->nf[0],
@@ -582,8 +620,8 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
     else nufft_default_opts(&o);
     if (!(o.L > 0) || (o.modeord != 0 && o.modeord != 1)) return NUFFT_ERR_ARG;
     if (o.spread_warps != 0 && o.spread_warps != 1 && o.spread_warps != 2 &&
-        o.spread_warps != 3 && o.spread_warps != 4 && o.spread_warps != 8 && o.spread_warps != -1 &&
-        o.spread_warps != -2)
+        o.spread_warps != 3 && o.spread_warps != 4 && o.spread_warps != 5 && o.spread_warps != 8 &&
+        o.spread_warps != -1 && o.spread_warps != -2)
         return NUFFT_ERR_ARG;
     if (o.interp_method < 0 || o.interp_method > 2) return NUFFT_ERR_ARG;
 
@@ -616,9 +654,18 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
     p->interp_method = o.interp_method;
 
     Geom& g = p->geom;
+    g.nsub = 1;
+    g.G = 0;
+    const bool sub = o.spread_warps == 5;  // sub-bin register-row spread (spread_sub.cu)
+    if (sub && !spread_sub_width(p->w)) {
+        delete p;
+        return NUFFT_ERR_UNSUPPORTED;
+    }
     for (int d = 0; d < 3; ++d) {
         g.nf[d] = p->nf[d];
-        int t = o.tile[d] > 0 ? o.tile[d] : default_tile(p->w, precision, p->nf[d]);
+        int t = o.tile[d] > 0 ? o.tile[d]
+                : sub         ? sub_default_tile(p->w, p->nf[d])
+                              : default_tile(p->w, precision, p->nf[d]);
         if (t < 1 || t > 255 || t + p->w + 2 > p->nf[d]) {
             delete p;
             return NUFFT_ERR_ARG;
@@ -626,6 +673,18 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
         g.T[d] = t;
         g.nb[d] = (int)((p->nf[d] + t - 1) / t);
         g.scale[d] = (double)p->nf[d] / o.L;
+    }
+    if (sub) {  // bins of ns_d sub-bins of G = 9 - w stencil bases: T_d + 1 = ns_d G
+        g.G = 9 - p->w;
+        g.nsub = 1;
+        for (int d = 0; d < 3; ++d) {
+            if ((g.T[d] + 1) % g.G) {
+                delete p;
+                return NUFFT_ERR_ARG;
+            }
+            g.ns[d] = (g.T[d] + 1) / g.G;
+            g.nsub *= g.ns[d];
+        }
     }
     g.L = o.L;
     g.w = p->w;
@@ -659,10 +718,13 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
             return NUFFT_ERR_CUDA;
         }
         const bool rows = g.spread_warps == 1, outer = g.spread_warps == 2 || g.spread_warps == 3;
+        const bool subk = g.spread_warps == 5;
         const bool auto_tile = o.tile[0] <= 0 && o.tile[1] <= 0 && o.tile[2] <= 0;
         for (;;) {
             const size_t sp =
-                precision == NUFFT_F64
+                subk ? (precision == NUFFT_F64 ? spread_sub_smem_bytes<double>(g)
+                                               : spread_sub_smem_bytes<float>(g))
+                : precision == NUFFT_F64
                     ? (outer  ? spread_outer_smem_bytes<double>(g)
                        : rows ? spread_rows_smem_bytes<double>(g)
                               : spread_smem_bytes<double>(g))
@@ -674,7 +736,19 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
             if (need <= (size_t)smem_max) break;
             // a built-in tile too large for one CTA (the widest kernels) shrinks to fit;
             // a caller's tile is refused
-            if (!auto_tile || outer || rows || g.T[0] <= 2) {
+            if (subk && auto_tile && g.nsub > 1) {  // one sub-bin less per axis
+                g.nsub = 1;
+                for (int d = 0; d < 3; ++d) {
+                    if (g.ns[d] > 1) {
+                        --g.ns[d];
+                        g.T[d] -= g.G;
+                    }
+                    g.nb[d] = (int)((p->nf[d] + g.T[d] - 1) / g.T[d]);
+                    g.nsub *= g.ns[d];
+                }
+                continue;
+            }
+            if (!auto_tile || outer || rows || subk || g.T[0] <= 2) {
                 delete p;
                 return NUFFT_ERR_ARG;
             }
@@ -715,9 +789,14 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
         // the complex 3D cuFFT plan (and its workspace) is created on the first complex
         // execute: a plan used only through the real transforms never holds it
     }
-    if (!st) st = dev_alloc(p, (void**)&p->count, sizeof(uint32_t) * (size_t)p->nbins);
+    // sort keys: bins, or (bin, sub-bin) pairs for the sub-bin spread
+    const int64_t nkeys = p->nbins * (int64_t)g.nsub;
+    if (!st && nkeys >= ((int64_t)1 << 31)) st = NUFFT_ERR_UNSUPPORTED;
+    if (!st) st = dev_alloc(p, (void**)&p->count, sizeof(uint32_t) * (size_t)nkeys);
     if (!st) st = dev_alloc(p, (void**)&p->offset, sizeof(uint32_t) * (size_t)(p->nbins + 1));
-    if (!st) st = dev_alloc(p, (void**)&p->blocksum, sizeof(uint32_t) * scan_blocksum_elems(p->nbins));
+    if (!st && g.nsub > 1)
+        st = dev_alloc(p, (void**)&p->offset_key, sizeof(uint32_t) * (size_t)(nkeys + 1));
+    if (!st) st = dev_alloc(p, (void**)&p->blocksum, sizeof(uint32_t) * scan_blocksum_elems(nkeys));
     if (!st && p->timing)
         for (int i = 0; i < 8; ++i) {
             cudaEventCreate(&p->ev0[i]);
@@ -1057,6 +1136,7 @@ int nufft_destroy(nufft_handle p) {
     dev_free(p, &p->d_grid, 0);
     dev_free(p, (void**)&p->count, 0);
     dev_free(p, (void**)&p->offset, 0);
+    dev_free(p, (void**)&p->offset_key, 0);
     dev_free(p, (void**)&p->blocksum, 0);
     dev_free(p, (void**)&p->bin_of, 0);
     dev_free(p, (void**)&p->rank_of, 0);

@@ -48,6 +48,7 @@ struct nufft_plan_s {
     int64_t cap = 0;
     uint32_t* count = nullptr;
     uint32_t* offset = nullptr;
+    uint32_t* offset_key = nullptr;  // (bin, sub-bin) starts when geom.nsub > 1
     uint32_t* blocksum = nullptr;
     uint32_t* bin_of = nullptr;   // setpts scratch when the grid buffer cannot host it
     uint32_t* rank_of = nullptr;

@@ -44,6 +44,39 @@ __device__ __forceinline__ int cell_of(double s, int64_t nf) {
     return (int)(c >= nf ? nf - 1 : c);
 }
 
+// Bin-local stencil record of one coordinate (reading R4: a = ceil(s - w/2)).
+//   r  = s - (bin origin)          exact in fp64
+//   ls = r + floor(w/2)            coordinate relative to the tile origin
+//   la = ceil(ls - w/2)            local stencil base, in [0, T]
+//   d  = ls - la                   phase offset, z_k = 2 (k - d) / w
+__device__ __forceinline__ void local_stencil(double s, int c, int T, int w, int* la, double* d) {
+    const int origin = (c / T) * T;
+    const double ls = (s - (double)origin) + (double)(w / 2);
+    const double a = ceil(ls - 0.5 * (double)w);
+    *la = (int)a;
+    *d = ls - a;
+}
+
+// Sub-bin of a point from its bin-local stencil bases (Geom::nsub > 1): the same
+// la the scatter stores, so the sub-bin kernel sees la - G * sub in [0, G).
+__device__ __forceinline__ uint32_t sub_of(const Geom& g, double sx, int cx, double sy, int cy,
+                                           double sz, int cz) {
+    int lax, lay, laz;
+    double dd;
+    local_stencil(sx, cx, g.T[0], g.w, &lax, &dd);
+    local_stencil(sy, cy, g.T[1], g.w, &lay, &dd);
+    local_stencil(sz, cz, g.T[2], g.w, &laz, &dd);
+    return (uint32_t)((laz / g.G * g.ns[1] + lay / g.G) * g.ns[0] + lax / g.G);
+}
+
+// slab-local z coordinate exactly as the scatter uses it (clamped into the slab)
+__device__ __forceinline__ double slab_z(const Geom& g, double szg) {
+    double sz = szg - (double)g.z_lo;
+    if (!(sz >= 0.0)) sz = 0.0;  // outside the slab: clamp (see bin_count_kernel)
+    if (sz >= (double)g.nz_loc) sz = (double)g.nz_loc - 0.5;
+    return sz;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kSortThreads) bin_count_kernel(
     Geom g, int64_t Np, const T* __restrict__ x, const T* __restrict__ y,
@@ -53,15 +86,23 @@ __global__ void __launch_bounds__(kSortThreads) bin_count_kernel(
          i += (int64_t)gridDim.x * blockDim.x) {
         uint32_t bin;
         {
-            int cx = cell_of(fold_rescale((double)x[i], g.L, g.scale[0], g.nf[0]), g.nf[0]);
-            int cy = cell_of(fold_rescale((double)y[i], g.L, g.scale[1], g.nf[1]), g.nf[1]);
-            int cz = cell_of(fold_rescale((double)z[i], g.L, g.scale[2], g.nf[2]), g.nf[2]) -
-                     (int)g.z_lo;
+            const double sx = fold_rescale((double)x[i], g.L, g.scale[0], g.nf[0]);
+            const double sy = fold_rescale((double)y[i], g.L, g.scale[1], g.nf[1]);
+            const double szg = fold_rescale((double)z[i], g.L, g.scale[2], g.nf[2]);
+            int cx = cell_of(sx, g.nf[0]);
+            int cy = cell_of(sy, g.nf[1]);
+            int cz = cell_of(szg, g.nf[2]) - (int)g.z_lo;
             // a slab plan given a point outside its slab (points_owned misuse): keep
             // memory safe by clamping to the slab (the caller's contract is broken)
             cz = cz < 0 ? 0 : (cz >= (int)g.nz_loc ? (int)g.nz_loc - 1 : cz);
             bin = (uint32_t)(cx / g.T[0]) +
                   (uint32_t)g.nb[0] * ((uint32_t)(cy / g.T[1]) + (uint32_t)g.nb[1] * (uint32_t)(cz / g.T[2]));
+            if (g.nsub > 1) {  // sort key = (bin, sub-bin), as the scatter's record
+                const double sz = slab_z(g, szg);
+                bin = bin * (uint32_t)g.nsub +
+                      sub_of(g, sx, cx, sy, cy, sz,
+                             cell_of(sz + (double)g.z_lo, g.nf[2]) - (int)g.z_lo);
+            }
         }
         // one atomicAdd per point: the rank of the point in its bin.  (A warp-
         // aggregated __match_any_sync version was measured slower on B200 for the
@@ -157,19 +198,6 @@ __global__ void __launch_bounds__(kScanThreads) scan_tiles(const uint32_t* __res
     if (blockIdx.x == gridDim.x - 1 && threadIdx.x == blockDim.x - 1) offset[n] = ex;
 }
 
-// Bin-local stencil record of one coordinate (reading R4: a = ceil(s - w/2)).
-//   r  = s - (bin origin)          exact in fp64
-//   ls = r + floor(w/2)            coordinate relative to the tile origin
-//   la = ceil(ls - w/2)            local stencil base, in [0, T]
-//   d  = ls - la                   phase offset, z_k = 2 (k - d) / w
-__device__ __forceinline__ void local_stencil(double s, int c, int T, int w, int* la, double* d) {
-    const int origin = (c / T) * T;
-    const double ls = (s - (double)origin) + (double)(w / 2);
-    const double a = ceil(ls - 0.5 * (double)w);
-    *la = (int)a;
-    *d = ls - a;
-}
-
 // one sorted record: two 16-byte streaming stores (.cs: written once, read by
 // the next kernel from HBM; do not keep it in L1)
 template <typename T>
@@ -215,9 +243,7 @@ __global__ void __launch_bounds__(kSortThreads) scatter_kernel(
             if (i >= Np) break;
             const double sx = fold_rescale((double)xv[u], g.L, g.scale[0], g.nf[0]);
             const double sy = fold_rescale((double)yv[u], g.L, g.scale[1], g.nf[1]);
-            double sz = fold_rescale((double)zv[u], g.L, g.scale[2], g.nf[2]) - (double)g.z_lo;
-            if (!(sz >= 0.0)) sz = 0.0;  // outside the slab: clamp (see bin_count_kernel)
-            if (sz >= (double)g.nz_loc) sz = (double)g.nz_loc - 0.5;
+            const double sz = slab_z(g, fold_rescale((double)zv[u], g.L, g.scale[2], g.nf[2]));
             int lax, lay, laz;
             double ddx, ddy, ddz;
             local_stencil(sx, cell_of(sx, g.nf[0]), g.T[0], g.w, &lax, &ddx);
@@ -268,6 +294,14 @@ __global__ void __launch_bounds__(kWThreads) weights_kernel(const PtRec<T>* __re
     }
 }
 
+// per-bin starts from the (bin, sub-bin) key starts: offset[b] = offset_key[b nsub]
+__global__ void bin_offsets_kernel(const uint32_t* __restrict__ offset_key, int64_t nbins,
+                                   int nsub, uint32_t* __restrict__ offset) {
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b <= nbins;
+         b += (int64_t)gridDim.x * blockDim.x)
+        offset[b] = offset_key[b * nsub];
+}
+
 inline int grid_for(int64_t n, int threads) {
     int64_t b = (n + threads - 1) / threads;
     const int64_t cap = 148 * 16;  // persistent-style cap: 16 resident CTAs per SM
@@ -281,9 +315,10 @@ size_t scan_blocksum_elems(int64_t nbins) { return (size_t)((nbins + kScanTile -
 
 template <typename T>
 cudaError_t launch_bin_sort(const Geom& g, int64_t Np, const T* x, const T* y, const T* z,
-                            uint32_t* count, uint32_t* offset, uint32_t* blocksum,
-                            uint32_t* bin_of, uint32_t* rank_of, PtRec<T>* rec, int64_t nbins,
-                            cudaStream_t s) {
+                            uint32_t* count, uint32_t* offset_key, uint32_t* offset,
+                            uint32_t* blocksum, uint32_t* bin_of, uint32_t* rank_of,
+                            PtRec<T>* rec, int64_t nbins_, cudaStream_t s) {
+    const int64_t nbins = nbins_ * (g.nsub > 1 ? g.nsub : 1);  // sort keys
     cudaError_t e = cudaMemsetAsync(count, 0, sizeof(uint32_t) * (size_t)nbins, s);
     if (e != cudaSuccess) return e;
     if (Np > 0) {
@@ -293,11 +328,14 @@ cudaError_t launch_bin_sort(const Geom& g, int64_t Np, const T* x, const T* y, c
     const int64_t ntiles = (nbins + kScanTile - 1) / kScanTile;
     scan_tile_sums<<<(unsigned)ntiles, kScanThreads, 0, s>>>(count, nbins, blocksum);
     scan_sums<<<1, kScanThreads, 0, s>>>(blocksum, ntiles);
-    scan_tiles<<<(unsigned)ntiles, kScanThreads, 0, s>>>(count, nbins, blocksum, offset);
+    scan_tiles<<<(unsigned)ntiles, kScanThreads, 0, s>>>(count, nbins, blocksum, offset_key);
     if (Np > 0) {
         scatter_kernel<T><<<grid_for(Np, kSortThreads), kSortThreads, 0, s>>>(
-            g, Np, x, y, z, bin_of, rank_of, offset, rec);
+            g, Np, x, y, z, bin_of, rank_of, offset_key, rec);
     }
+    if (g.nsub > 1)
+        bin_offsets_kernel<<<grid_for(nbins_ + 1, kSortThreads), kSortThreads, 0, s>>>(
+            offset_key, nbins_, g.nsub, offset);
     return cudaGetLastError();
 }
 
@@ -327,11 +365,11 @@ template cudaError_t launch_weights<double>(const PtRec<double>*, int64_t, int, 
                                             cudaStream_t);
 
 template cudaError_t launch_bin_sort<float>(const Geom&, int64_t, const float*, const float*,
-                                            const float*, uint32_t*, uint32_t*, uint32_t*,
+                                            const float*, uint32_t*, uint32_t*, uint32_t*, uint32_t*,
                                             uint32_t*, uint32_t*, PtRec<float>*, int64_t,
                                             cudaStream_t);
 template cudaError_t launch_bin_sort<double>(const Geom&, int64_t, const double*, const double*,
-                                             const double*, uint32_t*, uint32_t*, uint32_t*,
+                                             const double*, uint32_t*, uint32_t*, uint32_t*, uint32_t*,
                                              uint32_t*, uint32_t*, PtRec<double>*, int64_t,
                                              cudaStream_t);
 

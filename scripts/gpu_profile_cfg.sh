@@ -3,7 +3,7 @@
 TAG=${1:-dev}
 mkdir -p gpurun_out
 python -m paper_2605_10678_b200.build > gpurun_out/build_$TAG.log 2>&1 || { echo BUILD FAILED; exit 1; }
-ARGS="--config ${CONFIG:-c2b} --steps 2 --warmup 3 --no-cpu-baseline ${TILE:+--tile $TILE}"
+ARGS="--config ${CONFIG:-c2b} --steps 2 --warmup 3 --no-cpu-baseline --no-pif ${TILE:+--tile $TILE} ${EXTRA}"
 timeout 300 python bench.py $ARGS > gpurun_out/plain_$TAG.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py $ARGS > gpurun_out/ncu_launch_$TAG.log 2>&1; echo "ncu_launch=$?"
 if [ -n "$PROFILE" ]; then

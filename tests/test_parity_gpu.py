@@ -211,6 +211,51 @@ def test_every_spread_kernel(nb, prec, kernel, eps):
 
 
 @pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("eps", [1e-1, 1e-2, 1e-3, 1e-4, 1e-5])
+def test_sub_bin_spread_every_width(nb, prec, eps):
+    # spread_warps = 5: sub-bin register rows, w = 2 .. 6, default tile (T + 1 = ns G)
+    N, Np = (32, 24, 40), 40000
+    pts, c = host_inputs(Np, prec, seed=21)
+    fk = synthetic.modes(*N).to(c.dtype)
+    plan, g1, g2 = run_pair(nb, N, eps, prec, pts, c, fk, spread_warps=5)
+    w = plan.info()["w"]
+    G = 9 - w
+    assert all((t + 1) % G == 0 for t in plan.info()["tile"])
+    x, y, z = (np64(p) for p in pts)
+    assert err(g1, oracle.type1(x, y, z, np64(c), N, eps)) <= TOL[prec]
+    assert err(g2, oracle.type2(x, y, z, np64(fk), eps)) <= TOL[prec]
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_sub_bin_spread_tiles_clusters_precompute(nb, prec):
+    # ragged / non-cubic tiles, one-hot bins (every point in one cell), precomputed
+    # weights, Landau points on [0, 4 pi)^3 -- all against the oracle's spread
+    eps = 1e-4
+    N = (24, 20, 28)
+    G = 9 - nb.Plan((8, 8, 8), eps, precision=prec).info()["w"]
+    fk = synthetic.modes(*N)
+    cases = [dict(tile=(G - 1, 2 * G - 1, 3 * G - 1)), dict(precompute=1),
+             dict(tile=(3 * G - 1,) * 3, precompute=-1)]
+    for kind in ("uniform", "clustered", "one", "landau"):
+        L = 4 * math.pi if kind == "landau" else TWO_PI
+        if kind == "one":
+            pts = tuple(torch.full((3000,), 1.2345, dtype=torch.float64) for _ in range(3))
+            c = synthetic.strengths(3000)
+        else:
+            pts, c = host_inputs(25000, "f64", kind=kind, seed=22)
+        rdt = torch.float64 if prec == "f64" else torch.float32
+        pts = tuple(p.to(rdt) for p in pts)
+        c = c.to(torch.complex128 if prec == "f64" else torch.complex64)
+        x, y, z = (np64(p) for p in pts)
+        o1 = oracle.type1(x, y, z, np64(c), N, eps, L=L)
+        o2 = oracle.type2(x, y, z, np64(fk), eps, L=L)
+        for kw in cases:
+            _, g1, g2 = run_pair(nb, N, eps, prec, pts, c, fk.to(c.dtype), L=L, spread_warps=5, **kw)
+            assert err(g1, o1) <= TOL[prec], (kind, kw)
+            assert err(g2, o2) <= TOL[prec], (kind, kw)
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
 @pytest.mark.parametrize("kernel", [1, 2, 8])
 @pytest.mark.parametrize("precompute", [-1, 1])
 def test_precomputed_weights_both_paths(nb, prec, kernel, precompute):

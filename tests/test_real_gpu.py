@@ -42,12 +42,12 @@ def inputs(Np, prec, seed=1, L=2 * math.pi, kind="uniform"):
 
 
 @pytest.mark.parametrize("prec", ["f64", "f32"])
-@pytest.mark.parametrize("kernel", [2, 8])
+@pytest.mark.parametrize("kernel", [2, 5, 8])
 @pytest.mark.parametrize("iflag", [-1, 1])
 def test_real_type1_type2_vs_oracle(nb, prec, kernel, iflag):
-    eps = 1e-6
+    eps = 1e-5 if kernel == 5 else 1e-6  # sub-bin rows: w <= 6
     w = nb.Plan((8, 8, 8), eps, precision=prec).info()["w"]
-    tile = 16 - w if kernel == 2 else 8
+    tile = 16 - w if kernel == 2 else (None if kernel == 5 else 8)
     N, Np = (24, 20, 28), 30000
     pts, c = inputs(Np, prec, seed=21)
     cdt = torch.complex128 if prec == "f64" else torch.complex64
@@ -111,16 +111,17 @@ def test_real_pif_like_hermitian_field_and_edge_cases(nb):
 
 
 @pytest.mark.parametrize("prec", ["f64", "f32"])
-@pytest.mark.parametrize("eps", [1e-4, 1e-7])
-def test_three_field_gather_and_fused_kick(nb, prec, eps):
+@pytest.mark.parametrize("eps,kernel", [(1e-4, 0), (1e-7, 0), (1e-4, 5), (1e-5, 5)])
+def test_three_field_gather_and_fused_kick(nb, prec, eps, kernel):
     # type2_real3 == three type2_real calls; gather_kick == type2_real + kick per component
+    # (kernel 5: sub-bin sorted plan -> the register-block gather for all three paths)
     if prec == "f32" and eps < 1e-6:
         eps = 1e-6
     N, Np = (16, 20, 24), 20000
     pts, _ = inputs(Np, prec, seed=24)
     cdt = torch.complex128 if prec == "f64" else torch.complex64
     fks = [synthetic.modes(*N, seed=40 + d).to(cdt).cuda() for d in range(3)]
-    plan = nb.Plan(N, eps, precision=prec)
+    plan = nb.Plan(N, eps, precision=prec, spread_warps=kernel)
     plan.setpts(*(p.cuda() for p in pts))
     sep = torch.stack([plan.type2_real(f) for f in fks], dim=1)
     vec = plan.type2_real3(*fks)
