@@ -200,6 +200,14 @@ const char* nufft_strerror(int code);
 int nufft_comm_unique_id(char id[128]);                                    /* rank 0, host */
 int nufft_comm_init(const char id[128], int nranks, int rank, void** comm); /* collective   */
 int nufft_comm_destroy(void* comm);
+/* Loopback communicators: nranks handles comms[0 .. nranks-1] (host array, filled) on
+ * the CURRENT device, one per rank of a z-slab decomposition that runs entirely on one
+ * GPU.  Each rank's plan calls must be issued from its own host thread (the calls are
+ * collective: every exchange meets the other ranks' threads), on the rank's own
+ * stream; messages are device-to-device copies.  Same plan semantics and results as
+ * NCCL communicators at any nranks -- a test / validation transport, not a
+ * performance path.  Destroy each handle with nufft_comm_destroy after its plan. */
+int nufft_comm_init_loopback(int nranks, void** comms);
 /* This rank's [lo, hi) range of mode STORAGE indices per axis (x, y, z): the whole
  * N1 N2 N3 block on one GPU; on a slab plan all of x and z and the y-slab
  * [r N2/P, (r+1) N2/P).  fk arguments of a slab plan are that block, x fastest. */

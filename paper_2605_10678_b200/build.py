@@ -30,7 +30,7 @@ CU_FLAGS = ARCH + COMMON + ["--expt-relaxed-constexpr", "-Xptxas", "-v"]
 # developer instrumentation only (e.g. -DNUFFT_OUTER_PROF); never set for the product build
 CU_FLAGS += os.environ.get("NUFFT_EXTRA_NVCC_FLAGS", "").split()
 
-SOURCES = ["sort.cu", "spread.cu", "spread_rows.cu", "spread_outer.cu", "spread_sub.cu", "interp.cu", "interp_real.cu", "interp_vec3.cu",
+SOURCES = ["sort.cu", "xport.cpp", "spread.cu", "spread_rows.cu", "spread_outer.cu", "spread_sub.cu", "interp.cu", "interp_real.cu", "interp_vec3.cu",
            "elementwise.cu", "pif.cu", "variants.cu", "spread_tc.cu", "dist_kernels.cu", "peak.cu", "plan.cpp", "dist.cpp"]
 
 

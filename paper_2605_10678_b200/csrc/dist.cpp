@@ -5,7 +5,8 @@
 // ACCUMULATED into the owners after spreading and FILLED from the owners before
 // interpolation, and the FFT is a distributed FFT.  On one NVSwitch box we use
 // z-slabs: rank r owns fine planes [r nf3/P, (r+1) nf3/P) and the
-// points whose fine cell lies there.
+// points whose fine cell lies there.  Every exchange goes through the communicator's
+// transport (xport.h): NCCL between GPUs, or loopback for P ranks on one GPU (tests).
 //
 //   setpts   owner = slab of the fine z-cell; counts all-to-all; points moved
 //            with grouped ncclSend/ncclRecv (skipped with opts.points_owned);
@@ -24,7 +25,6 @@
 // [r N2/P, (r+1) N2/P) along y (all of x and z), x fastest (nufft_local_modes).
 #include <cuda_runtime.h>
 #include <cufft.h>
-#include <nccl.h>
 
 #include <algorithm>
 #include <cstring>
@@ -32,9 +32,12 @@
 #include <vector>
 
 #include "plan_state.h"
+#include "xport.h"
 
+// a communicator: the transport (NCCL, or loopback for P ranks on one GPU) and
+// this handle's rank
 struct NufftComm {
-    ncclComm_t nccl = nullptr;
+    nufft::Xport* x = nullptr;
     int nranks = 1;
     int rank = 0;
 };
@@ -48,8 +51,8 @@ struct DistState {
     int64_t y0 = 0;      // first y storage index of this rank
     int hlo = 0, hhi = 0;
     int64_t plane = 0;   // nf1 nf2
-    ncclComm_t nccl = nullptr;
-    ncclDataType_t real_t = ncclDouble;
+    Xport* x = nullptr;  // the communicator's transport (xport.h)
+    size_t rs = 8;       // bytes per real
 
     void* xbuf = nullptr;      // nzl N2 N1 complex: x-y-truncated planes / z-lines (two roles)
     void* ybuf = nullptr;      // same size
@@ -89,13 +92,7 @@ struct DistState {
 
 namespace {
 
-int nccl_status(ncclResult_t r) { return r == ncclSuccess ? NUFFT_OK : NUFFT_ERR_NCCL; }
 
-#define NCK(expr)                                              \
-    do {                                                       \
-        ncclResult_t r__ = (expr);                             \
-        if (r__ != ncclSuccess) return NUFFT_ERR_NCCL;         \
-    } while (0)
 
 // grow-only staging buffers with 12.5 % slack: per-step particle migration changes
 // the counts slightly, and a cudaFree/cudaMalloc of GBs every step would dominate
@@ -114,17 +111,17 @@ int alltoallv(DistState* d, const void* send, const std::vector<unsigned long lo
               const std::vector<unsigned long long>& so, void* recv,
               const std::vector<unsigned long long>& rc, const std::vector<unsigned long long>& ro,
               size_t elem, cudaStream_t s) {
-    NCK(ncclGroupStart());
+    int st;
+    if ((st = d->x->group_start())) return st;
     for (int q = 0; q < d->P; ++q) {
-        if (sc[q])
-            NCK(ncclSend(static_cast<const char*>(send) + so[q] * elem, sc[q] * elem, ncclChar, q,
-                         d->nccl, s));
-        if (rc[q])
-            NCK(ncclRecv(static_cast<char*>(recv) + ro[q] * elem, rc[q] * elem, ncclChar, q,
-                         d->nccl, s));
+        if (sc[q] && (st = d->x->send(static_cast<const char*>(send) + so[q] * elem, sc[q] * elem,
+                                      q, s)))
+            return st;
+        if (rc[q] &&
+            (st = d->x->recv(static_cast<char*>(recv) + ro[q] * elem, rc[q] * elem, q, s)))
+            return st;
     }
-    NCK(ncclGroupEnd());
-    return NUFFT_OK;
+    return d->x->group_end(s);
 }
 
 // Ghost planes of the slab grid whose cells hold K reals (K = 2: complex, 1: real).
@@ -135,14 +132,17 @@ int halo_accumulate(nufft_plan_s* p, void* grid0, int K) {
     T* g0 = static_cast<T*>(grid0);
     const int prev = (d->r + d->P - 1) % d->P, next = (d->r + 1) % d->P;
     const size_t pl = (size_t)d->plane * K;  // reals per plane
-    NCK(ncclGroupStart());
+    const size_t rs = sizeof(T);
+    int st;
+    Xport* x = d->x;
+    if ((st = x->group_start())) return st;
     // my lower halo (hlo planes below plane 0) belongs to prev's top owned planes
-    NCK(ncclSend(g0 - d->hlo * pl, d->hlo * pl, d->real_t, prev, d->nccl, p->stream));
-    NCK(ncclRecv(d->halo_a, d->hlo * pl, d->real_t, next, d->nccl, p->stream));
+    if ((st = x->send(g0 - d->hlo * pl, d->hlo * pl * rs, prev, p->stream))) return st;
+    if ((st = x->recv(d->halo_a, d->hlo * pl * rs, next, p->stream))) return st;
     // my upper halo (hhi planes above the slab) belongs to next's bottom owned planes
-    NCK(ncclSend(g0 + d->nzl * pl, d->hhi * pl, d->real_t, next, d->nccl, p->stream));
-    NCK(ncclRecv(d->halo_b, d->hhi * pl, d->real_t, prev, d->nccl, p->stream));
-    NCK(ncclGroupEnd());
+    if ((st = x->send(g0 + d->nzl * pl, d->hhi * pl * rs, next, p->stream))) return st;
+    if ((st = x->recv(d->halo_b, d->hhi * pl * rs, prev, p->stream))) return st;
+    if ((st = x->group_end(p->stream))) return st;
     // the adds run on complex pairs (plane sizes are even)
     NUFFT_CK(launch_halo_add<T>((int64_t)(d->hlo * pl / 2),
                                 reinterpret_cast<C*>(g0 + (d->nzl - d->hlo) * pl),
@@ -157,15 +157,17 @@ int halo_fill(nufft_plan_s* p, void* grid0, int K) {
     T* g0 = static_cast<T*>(grid0);
     const int prev = (d->r + d->P - 1) % d->P, next = (d->r + 1) % d->P;
     const size_t pl = (size_t)d->plane * K;
-    NCK(ncclGroupStart());
+    const size_t rs = sizeof(T);
+    int st;
+    Xport* x = d->x;
+    if ((st = x->group_start())) return st;
     // my bottom hhi owned planes are prev's upper halo; next's bottom planes are mine
-    NCK(ncclSend(g0, d->hhi * pl, d->real_t, prev, d->nccl, p->stream));
-    NCK(ncclRecv(g0 + d->nzl * pl, d->hhi * pl, d->real_t, next, d->nccl, p->stream));
+    if ((st = x->send(g0, d->hhi * pl * rs, prev, p->stream))) return st;
+    if ((st = x->recv(g0 + d->nzl * pl, d->hhi * pl * rs, next, p->stream))) return st;
     // my top hlo owned planes are next's lower halo; prev's top planes fill my lower halo
-    NCK(ncclSend(g0 + (d->nzl - d->hlo) * pl, d->hlo * pl, d->real_t, next, d->nccl, p->stream));
-    NCK(ncclRecv(g0 - d->hlo * pl, d->hlo * pl, d->real_t, prev, d->nccl, p->stream));
-    NCK(ncclGroupEnd());
-    return NUFFT_OK;
+    if ((st = x->send(g0 + (d->nzl - d->hlo) * pl, d->hlo * pl * rs, next, p->stream))) return st;
+    if ((st = x->recv(g0 - d->hlo * pl, d->hlo * pl * rs, prev, p->stream))) return st;
+    return x->group_end(p->stream);
 }
 int fft_exec(nufft_plan_s* p, cufftHandle h, void* data, int sign) {
     const int dir = sign < 0 ? CUFFT_FORWARD : CUFFT_INVERSE;
@@ -194,8 +196,9 @@ int type1_t(nufft_plan_s* p, const void* c_local, void* fk_local) {
         if ((st = fft_exec(p, d->fft2, p->grid0, p->iflag))) return st;            // F (x, y)
         NUFFT_CK(launch_xy_pack<T>(static_cast<const C*>(p->grid0), p->nf, d->nzl, p->N, d->P,
                                    p->modeord, static_cast<C*>(d->xbuf), p->stream));  // chi (x, y)
-        NCK(ncclAlltoAll(d->xbuf, d->ybuf, 2 * (size_t)(d->nzl * d->NY * p->N[0]), d->real_t,
-                         d->nccl, p->stream));                                     // transpose
+        if ((st = d->x->alltoall(d->xbuf, d->ybuf, 2 * (size_t)(d->nzl * d->NY * p->N[0]) * d->rs,
+                                 p->stream)))
+            return st;                                                             // transpose
         if ((st = fft_exec(p, d->fft1, d->ybuf, p->iflag))) return st;             // F (z)
     }
     StageTimer tm(p, EV_DECONV);
@@ -221,8 +224,9 @@ int type2_t(nufft_plan_s* p, const void* fk_local, void* c_local) {
     {
         StageTimer tm(p, EV_FFT);
         if ((st = fft_exec(p, d->fft1, d->ybuf, -p->iflag))) return st;            // F^-1 (z)
-        NCK(ncclAlltoAll(d->ybuf, d->xbuf, 2 * (size_t)(d->nzl * d->NY * p->N[0]), d->real_t,
-                         d->nccl, p->stream));                                     // transpose
+        if ((st = d->x->alltoall(d->ybuf, d->xbuf, 2 * (size_t)(d->nzl * d->NY * p->N[0]) * d->rs,
+                                 p->stream)))
+            return st;                                                             // transpose
         NUFFT_CK(launch_xy_unpad<T>(static_cast<const C*>(d->xbuf), p->nf, d->nzl, p->N, d->P,
                                     p->modeord, static_cast<C*>(p->grid0), p->stream));  // chi^T
         if ((st = fft_exec(p, d->fft2, p->grid0, -p->iflag))) return st;           // F^-1 (x, y)
@@ -305,8 +309,9 @@ int type1_real_t(nufft_plan_s* p, const void* c_local, void* fk_local) {
         if (r != CUFFT_SUCCESS) return NUFFT_ERR_CUFFT;
         NUFFT_CK(launch_xy_pack_half<T>(static_cast<const C*>(d->hbuf), p->nf, d->nzl, p->N, d->P,
                                         p->modeord, static_cast<C*>(d->xbuf), p->stream));
-        NCK(ncclAlltoAll(d->xbuf, d->ybuf, 2 * (size_t)(d->nzl * d->NY * H1), d->real_t, d->nccl,
-                         p->stream));                                               // transpose
+        if ((st = d->x->alltoall(d->xbuf, d->ybuf, 2 * (size_t)(d->nzl * d->NY * H1) * d->rs,
+                                 p->stream)))
+            return st;                                                              // transpose
         if ((st = fft_exec(p, d->fft1h, d->ybuf, -1))) return st;                   // F (z), sign -
     }
     StageTimer tm(p, EV_DECONV);
@@ -339,8 +344,9 @@ int type2_real_t(nufft_plan_s* p, const void* fk_local, void* c_local) {
     {
         StageTimer tm(p, EV_FFT);
         if ((st = fft_exec(p, d->fft1h, d->ybuf, +1))) return st;                   // F^-1 (z)
-        NCK(ncclAlltoAll(d->ybuf, d->xbuf, 2 * (size_t)(d->nzl * d->NY * H1), d->real_t, d->nccl,
-                         p->stream));                                               // transpose
+        if ((st = d->x->alltoall(d->ybuf, d->xbuf, 2 * (size_t)(d->nzl * d->NY * H1) * d->rs,
+                                 p->stream)))
+            return st;                                                              // transpose
         NUFFT_CK(launch_xy_unpad_half<T>(static_cast<const C*>(d->xbuf), p->nf, d->nzl, p->N,
                                          d->P, p->modeord, static_cast<C*>(d->hbuf), p->stream));
         const cufftResult r =
@@ -369,8 +375,8 @@ int dist_init(nufft_plan_s* p) {
     p->dist = d;
     d->P = P;
     d->r = r;
-    d->nccl = cm->nccl;
-    d->real_t = p->prec == NUFFT_F64 ? ncclDouble : ncclFloat;
+    d->x = cm->x;
+    d->rs = p->real_size;
     d->nzl = p->nf[2] / P;
     d->NY = p->N[1] / P;
     d->y0 = (int64_t)r * d->NY;
@@ -387,7 +393,13 @@ int dist_init(nufft_plan_s* p) {
     g.hz_lo = d->hlo;
     g.hz_hi = d->hhi;
     if (g.T[2] > d->nzl) {
-        g.T[2] = (int)d->nzl;
+        if (g.nsub > 1) {  // sub-bin plans keep T + 1 = ns G: drop whole sub-bins in z
+            g.ns[2] = std::max(1, (int)((d->nzl + 1) / g.G));
+            g.T[2] = g.ns[2] * g.G - 1;
+            g.nsub = g.ns[0] * g.ns[1] * g.ns[2];
+        } else {
+            g.T[2] = (int)d->nzl;
+        }
         // rows / outer products need T = 16 - w on every axis
         if (g.spread_warps >= 1 && g.spread_warps <= 3) g.spread_warps = 8;
     }
@@ -461,7 +473,10 @@ static int agree(nufft_plan_s* p, int local) {
     unsigned long long flag = local >= 2 ? 1ull : 0ull;
     unsigned long long* f = d->d_mig + d->P + 2;
     NUFFT_CK(cudaMemcpyAsync(f, &flag, sizeof(flag), cudaMemcpyHostToDevice, p->stream));
-    NCK(ncclAllReduce(f, f, 1, ncclUint64, ncclMax, d->nccl, p->stream));
+    {
+        const int e = d->x->allreduce_max_u64(f, p->stream);
+        if (e) return e;
+    }
     NUFFT_CK(cudaMemcpyAsync(&flag, f, sizeof(flag), cudaMemcpyDeviceToHost, p->stream));
     NUFFT_CK(cudaStreamSynchronize(p->stream));
     if (local >= 2) return local;
@@ -501,7 +516,11 @@ int dist_setpts(nufft_plan_s* p, int64_t Np, const void* x, const void* y, const
         NUFFT_CK(launch_owner_count<float>(Np, static_cast<const float*>(z), g.L, g.scale[2],
                                            p->nf[2], (int)d->nzl, d->owner, d->rank_in,
                                            d->d_counts, p->stream));
-    NCK(ncclAlltoAll(d->d_counts, d->d_rcounts, 1, ncclUint64, d->nccl, p->stream));
+    {
+        const int e = d->x->alltoall(d->d_counts, d->d_rcounts, sizeof(unsigned long long),
+                                     p->stream);
+        if (e) return e;
+    }
     NUFFT_CK(cudaMemcpyAsync(d->scount.data(), d->d_counts, sizeof(unsigned long long) * P,
                              cudaMemcpyDeviceToHost, p->stream));
     NUFFT_CK(cudaMemcpyAsync(d->rcount.data(), d->d_rcounts, sizeof(unsigned long long) * P,
@@ -536,18 +555,20 @@ int dist_setpts(nufft_plan_s* p, int64_t Np, const void* x, const void* y, const
         NUFFT_CK(launch_pack_bytes(Np, (int)rs, src[k], d->owner, d->rank_in, d->d_off, sb, false,
                                    p->stream));
     }
-    NCK(ncclGroupStart());
+    if ((st = d->x->group_start())) return st;
     for (int k = 0; k < 3; ++k) {
         const char* sb = static_cast<const char*>(d->sbuf) + (size_t)k * Np * rs;
         char* rb = static_cast<char*>(d->rbuf) + (size_t)k * d->np_local * rs;
         for (int q = 0; q < P; ++q) {
-            if (d->scount[q])
-                NCK(ncclSend(sb + d->soff[q] * rs, d->scount[q] * rs, ncclChar, q, d->nccl, p->stream));
-            if (d->rcount[q])
-                NCK(ncclRecv(rb + d->roff[q] * rs, d->rcount[q] * rs, ncclChar, q, d->nccl, p->stream));
+            if (d->scount[q] &&
+                (st = d->x->send(sb + d->soff[q] * rs, d->scount[q] * rs, q, p->stream)))
+                return st;
+            if (d->rcount[q] &&
+                (st = d->x->recv(rb + d->roff[q] * rs, d->rcount[q] * rs, q, p->stream)))
+                return st;
         }
     }
-    NCK(ncclGroupEnd());
+    if ((st = d->x->group_end(p->stream))) return st;
     const char* rb = static_cast<const char*>(d->rbuf);
     st = local_sort(p, d->np_local, rb, rb + (size_t)d->np_local * rs,
                     rb + 2 * (size_t)d->np_local * rs);
@@ -704,7 +725,11 @@ int migrate_t(nufft_plan_s* p, int64_t* np, int64_t cap, T* const st[6]) {
     NUFFT_CK(cudaMemsetAsync(d->d_counts, 0, sizeof(unsigned long long) * P, p->stream));
     NUFFT_CK(launch_migrate_count<T>(n, st[2], g.L, g.scale[2], p->nf[2], (int)d->nzl, d->r,
                                      d->d_counts, p->stream));
-    NCK(ncclAlltoAll(d->d_counts, d->d_rcounts, 1, ncclUint64, d->nccl, p->stream));
+    {
+        const int e = d->x->alltoall(d->d_counts, d->d_rcounts, sizeof(unsigned long long),
+                                     p->stream);
+        if (e) return e;
+    }
     NUFFT_CK(cudaMemcpyAsync(d->scount.data(), d->d_counts, sizeof(unsigned long long) * P,
                              cudaMemcpyDeviceToHost, p->stream));
     NUFFT_CK(cudaMemcpyAsync(d->rcount.data(), d->d_rcounts, sizeof(unsigned long long) * P,
@@ -734,16 +759,19 @@ int migrate_t(nufft_plan_s* p, int64_t* np, int64_t cap, T* const st[6]) {
     NUFFT_CK(launch_migrate_move<T>(n, nleave, nrecv, st, g.L, g.scale[2], p->nf[2], (int)d->nzl,
                                     d->r, d->d_off, d->d_mig, send, recv, idx, idx + nleave,
                                     idx + 2 * nleave, d->d_mig + P, 0, p->stream));
-    NCK(ncclGroupStart());
-    for (int q = 0; q < P; ++q) {
-        if (d->scount[q])
-            NCK(ncclSend(send + 6 * d->soff[q], 6 * d->scount[q] * rs, ncclChar, q, d->nccl,
-                         p->stream));
-        if (d->rcount[q])
-            NCK(ncclRecv(recv + 6 * d->roff[q], 6 * d->rcount[q] * rs, ncclChar, q, d->nccl,
-                         p->stream));
+    {
+        int e;
+        if ((e = d->x->group_start())) return e;
+        for (int q = 0; q < P; ++q) {
+            if (d->scount[q] &&
+                (e = d->x->send(send + 6 * d->soff[q], 6 * d->scount[q] * rs, q, p->stream)))
+                return e;
+            if (d->rcount[q] &&
+                (e = d->x->recv(recv + 6 * d->roff[q], 6 * d->rcount[q] * rs, q, p->stream)))
+                return e;
+        }
+        if ((e = d->x->group_end(p->stream))) return e;
     }
-    NCK(ncclGroupEnd());
     NUFFT_CK(launch_migrate_move<T>(n, nleave, nrecv, st, g.L, g.scale[2], p->nf[2], (int)d->nzl,
                                     d->r, d->d_off, d->d_mig, send, recv, idx, idx + nleave,
                                     idx + 2 * nleave, d->d_mig + P, 1, p->stream));
@@ -773,20 +801,17 @@ int nufft_pif_migrate(nufft_handle p, int64_t* np, int64_t cap, void* x, void* y
 
 int nufft_comm_unique_id(char id[128]) {
     if (!id) return NUFFT_ERR_ARG;
-    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
-    ncclUniqueId u;
-    if (ncclGetUniqueId(&u) != ncclSuccess) return NUFFT_ERR_NCCL;
-    std::memcpy(id, &u, 128);
-    return NUFFT_OK;
+    int st = NUFFT_OK;
+    nufft::xport_nccl_unique_id(id, &st);
+    return st;
 }
 
 int nufft_comm_init(const char id[128], int nranks, int rank, void** comm) {
     if (!id || !comm || nranks < 1 || rank < 0 || rank >= nranks) return NUFFT_ERR_ARG;
     NufftComm* c = new (std::nothrow) NufftComm();
     if (!c) return NUFFT_ERR_ALLOC;
-    ncclUniqueId u;
-    std::memcpy(&u, id, 128);
-    if (ncclCommInitRank(&c->nccl, nranks, u, rank) != ncclSuccess) {
+    c->x = nufft::xport_nccl(id, nranks, rank);
+    if (!c->x) {
         delete c;
         return NUFFT_ERR_NCCL;
     }
@@ -796,12 +821,32 @@ int nufft_comm_init(const char id[128], int nranks, int rank, void** comm) {
     return NUFFT_OK;
 }
 
+int nufft_comm_init_loopback(int nranks, void** comms) {
+    if (!comms || nranks < 1) return NUFFT_ERR_ARG;
+    std::vector<nufft::Xport*> xs((size_t)nranks, nullptr);
+    int st = nufft::xport_loopback(nranks, xs.data());
+    if (st) return st;
+    for (int q = 0; q < nranks; ++q) {
+        NufftComm* c = new (std::nothrow) NufftComm();
+        if (!c) {
+            for (int k = 0; k < q; ++k) delete static_cast<NufftComm*>(comms[k]);
+            for (auto* x : xs) delete x;
+            return NUFFT_ERR_ALLOC;
+        }
+        c->x = xs[(size_t)q];
+        c->nranks = nranks;
+        c->rank = q;
+        comms[q] = c;
+    }
+    return NUFFT_OK;
+}
+
 int nufft_comm_destroy(void* comm) {
     if (!comm) return NUFFT_OK;
     NufftComm* c = static_cast<NufftComm*>(comm);
-    int st = c->nccl ? nufft::nccl_status(ncclCommDestroy(c->nccl)) : NUFFT_OK;
+    delete c->x;  // NCCL: ncclCommDestroy; loopback: this rank's events
     delete c;
-    return st;
+    return NUFFT_OK;
 }
 
 }  // extern "C"

@@ -107,11 +107,13 @@ __device__ __forceinline__ void run_points(V (&acc)[2][kBlk], const unsigned (&d
                                            const T* swz, int ry, int rz) {
     if constexpr (D < G) {
         unsigned msk = dmask[D] & run;
+        const T* wyp = swy + ry;
+        const T* wzp = swz + rz;
         while (msk) {
             const int j = __ffs(msk) - 1;
             msk &= msk - 1;
-            const T wyv = swy[j * kYS + ry];
-            const T f0 = wyv * swz[j * kYS + rz], f1 = wyv * swz[j * kYS + rz + 4];
+            const T wyv = wyp[j * kYS];
+            const T f0 = wyv * wzp[j * kYS], f1 = wyv * wzp[j * kYS + 4];
             fma_rows<V, T, W, D>(acc, sb + j * W, f0, f1);
         }
         run_points<V, T, W, G, D + 1>(acc, dmask, run, sb, swy, swz, ry, rz);
@@ -185,7 +187,6 @@ __global__ void __launch_bounds__(32 * NW, 1)
     const uint32_t wbeg = beg + (uint32_t)(((uint64_t)n * warp) / NW);
     const uint32_t wend = beg + (uint32_t)(((uint64_t)n * (warp + 1)) / NW);
     const int ry = lane & 7, rz = lane >> 3;  // this lane's rows: (ry, rz) and (ry, rz + 4)
-    const T two_over_w = (T)2 / (T)W;
     int cur = -1;  // sub-bin whose block the registers hold
     V acc[2][kBlk];
 #pragma unroll
@@ -205,6 +206,17 @@ __global__ void __launch_bounds__(32 * NW, 1)
             my_dx = lx - sx * G;
             my_sub = sx | (sy << 8) | (sz << 16);
             const V cv = c[rr.perm];
+            T wt[3][W];
+            if (p.w) {  // precomputed at setpts (opts.precompute)
+                const T* pw = p.w + (size_t)(c0 + lane) * (3 * W);
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+#pragma unroll
+                    for (int k = 0; k < W; ++k) wt[a][k] = pw[a * W + k];
+            } else {
+                const T dd[3] = {rr.d[0], rr.d[1], rr.d[2]};
+                es_weights3<T, W>(dd, beta, tab, wt);
+            }
             T* wyl = swy + lane * kYS;
             T* wzl = swz + lane * kYS;
 #pragma unroll
@@ -212,22 +224,11 @@ __global__ void __launch_bounds__(32 * NW, 1)
                 wyl[k] = (T)0;
                 wzl[k] = (T)0;
             }
-            if (p.w) {  // precomputed at setpts (opts.precompute)
-                const T* pw = p.w + (size_t)(c0 + lane) * (3 * W);
 #pragma unroll
-                for (int k = 0; k < W; ++k) {
-                    sb[lane * W + k] = vscale(cv, pw[k]);
-                    wyl[dy + k] = pw[W + k];
-                    wzl[dz + k] = pw[2 * W + k];
-                }
-            } else {
-#pragma unroll
-                for (int k = 0; k < W; ++k) {
-                    sb[lane * W + k] =
-                        vscale(cv, es_weight_tab<T>(((T)k - rr.d[0]) * two_over_w, beta, tab));
-                    wyl[dy + k] = es_weight_tab<T>(((T)k - rr.d[1]) * two_over_w, beta, tab);
-                    wzl[dz + k] = es_weight_tab<T>(((T)k - rr.d[2]) * two_over_w, beta, tab);
-                }
+            for (int k = 0; k < W; ++k) {
+                sb[lane * W + k] = vscale(cv, wt[0][k]);
+                wyl[dy + k] = wt[1][k];
+                wzl[dz + k] = wt[2][k];
             }
         }
         unsigned dmask[G];
@@ -363,7 +364,6 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW)
     const uint32_t wbeg = beg + (uint32_t)(((uint64_t)n * warp) / NW);
     const uint32_t wend = beg + (uint32_t)(((uint64_t)n * (warp + 1)) / NW);
     const int ry = lane & 7, rz = lane >> 3;
-    const T two_over_w = (T)2 / (T)W;
     int cur = -1;
     V acc[2][kBlk];
 #pragma unroll
@@ -383,6 +383,17 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW)
             my_dx = lx - sx * G;
             my_sub = sx | (sy << 8) | (sz << 16);
             const V cv = c[rr.perm];
+            T wt[3][W];
+            if (p.w) {  // precomputed at setpts (opts.precompute)
+                const T* pw = p.w + (size_t)(c0 + lane) * (3 * W);
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+#pragma unroll
+                    for (int k = 0; k < W; ++k) wt[a][k] = pw[a * W + k];
+            } else {
+                const T dd[3] = {rr.d[0], rr.d[1], rr.d[2]};
+                es_weights3<T, W>(dd, beta, tab, wt);
+            }
             T* wyl = swy + lane * kYS;
             T* wzl = swz + lane * kYS;
 #pragma unroll
@@ -390,22 +401,11 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW)
                 wyl[k] = (T)0;
                 wzl[k] = (T)0;
             }
-            if (p.w) {
-                const T* pw = p.w + (size_t)(c0 + lane) * (3 * W);
 #pragma unroll
-                for (int k = 0; k < W; ++k) {
-                    sb[lane * W + k] = vscale(cv, pw[k]);
-                    wyl[dy + k] = pw[W + k];
-                    wzl[dz + k] = pw[2 * W + k];
-                }
-            } else {
-#pragma unroll
-                for (int k = 0; k < W; ++k) {
-                    sb[lane * W + k] =
-                        vscale(cv, es_weight_tab<T>(((T)k - rr.d[0]) * two_over_w, beta, tab));
-                    wyl[dy + k] = es_weight_tab<T>(((T)k - rr.d[1]) * two_over_w, beta, tab);
-                    wzl[dz + k] = es_weight_tab<T>(((T)k - rr.d[2]) * two_over_w, beta, tab);
-                }
+            for (int k = 0; k < W; ++k) {
+                sb[lane * W + k] = vscale(cv, wt[0][k]);
+                wyl[dy + k] = wt[1][k];
+                wzl[dz + k] = wt[2][k];
             }
         }
         unsigned dmask[G];

@@ -87,5 +87,19 @@ template <> __device__ __forceinline__ double es_weight_tab<double>(double zz, d
     return t >= 0.0 ? e : 0.0;
 }
 
+// The 3w weights of one point, phi(2 (k - d_a) / w) for axis a and node k, into
+// registers.  All table reads happen here, before the caller's shared-memory
+// stores: a store that may alias the table would otherwise order every later
+// evaluation after it and serialise the 3w independent chains.
+template <typename T, int W>
+__device__ __forceinline__ void es_weights3(const T (&d)[3], T beta, const double* tab,
+                                            T (&w)[3][W]) {
+    const T two_over_w = (T)2 / (T)W;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int k = 0; k < W; ++k) w[a][k] = es_weight_tab<T>(((T)k - d[a]) * two_over_w, beta, tab);
+}
+
 }  // namespace dev
 }  // namespace nufft

@@ -67,7 +67,8 @@ _EXPORTS = ["nufft_default_opts", "nufft_plan", "nufft_setpts", "nufft_execute_t
             "nufft_comm_destroy", "nufft_local_modes", "nufft_pif_poisson", "nufft_pif_kick",
             "nufft_pif_drift", "nufft_pif_migrate", "nufft_execute_type1_real",
             "nufft_execute_type2_real", "nufft_pif_kick_real", "nufft_pif_poisson_real",
-            "nufft_execute_type2_real3", "nufft_pif_gather_kick", "nufft_fma_peak"]
+            "nufft_execute_type2_real3", "nufft_pif_gather_kick", "nufft_fma_peak",
+            "nufft_comm_init_loopback"]
 
 _lib = None
 
@@ -96,6 +97,7 @@ def lib():
         L.nufft_comm_init.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_int,
                                       ctypes.POINTER(vp)]
         L.nufft_comm_destroy.argtypes = [vp]
+        L.nufft_comm_init_loopback.argtypes = [ctypes.c_int, ctypes.POINTER(vp)]
         L.nufft_pif_poisson.argtypes = [vp, vp, vp, vp, vp]
         L.nufft_pif_poisson_real.argtypes = [vp, vp, vp, vp, vp]
         L.nufft_execute_type2_real3.argtypes = [vp, vp, vp, vp, vp]
@@ -152,6 +154,20 @@ class Comm:
         if getattr(self, "_h", None):
             lib().nufft_comm_destroy(self._h)
             self._h = None
+
+    @classmethod
+    def loopback(cls, nranks: int):
+        """nranks loopback communicators on the current GPU (nufft_comm_init_loopback):
+        rank r's plan must be driven from its own host thread.  For tests of the
+        z-slab path at any rank count on one device."""
+        hs = (ctypes.c_void_p * nranks)()
+        _check(lib().nufft_comm_init_loopback(nranks, hs), "nufft_comm_init_loopback")
+        out = []
+        for r in range(nranks):
+            c = cls.__new__(cls)
+            c.rank, c.size, c._h = r, nranks, ctypes.c_void_p(hs[r])
+            out.append(c)
+        return out
 
 
 def fma_peak(precision="f64", stream=None) -> float:
