@@ -277,7 +277,8 @@ def run_ours(args, cfg):
     plan = nb.Plan(N, cfg["eps"], precision=cfg["prec"], timing=True, device=device,
                    tile=args.tile, spread_warps=args.spread_warps, comm=comm,
                    points_owned=ws > 1, interp_method=args.interp_method,
-                   precompute=args.precompute, L=cfg.get("L", 2 * math.pi))
+                   precompute=args.precompute, L=cfg.get("L", 2 * math.pi),
+                   fft_method=args.fft_method if ws == 1 else 0)
     pts, c, fk = make_inputs(cfg, rank, ws, device, plan.local_modes() if ws > 1 else None)
     Np = pts[0].numel()
     if args.real:  # real strengths / outputs: the R2C / C2R path
@@ -405,7 +406,7 @@ def run_ours(args, cfg):
                        "L": cfg.get("L", 2 * math.pi),
                        "w": info["w"], "precision": cfg["prec"], "points": cfg["kind"],
                        "tile": info["tile"],
-                       "kernels": {"spread_warps": args.spread_warps,
+                       "kernels": {"spread_warps": args.spread_warps, "fft_method": args.fft_method,
                                    "interp_method": args.interp_method,
                                    "weights_precomputed": info["weights_precomputed"]},
                        "values": "real (R2C / C2R)" if args.real else "complex",
@@ -691,6 +692,8 @@ def main():
                     help="spread kernel: 1 rows, 2 outer products, 4 / 8 smem planes (default: built-in)")
     ap.add_argument("--precompute", type=int, default=0,
                     help="per-point ES weight table: 0 auto (fp64), 1 always, -1 never")
+    ap.add_argument("--fft-method", type=int, default=0,
+                    help="1: the paper's pruned sigma = 2 FFT (eight N^3 parity sub-grid FFTs)")
     ap.add_argument("--interp-method", type=int, default=0,
                     help="ablation: 1 / 2 = the paper's Direct Interpolation, caller / sorted order")
     ap.add_argument("--real", action="store_true",

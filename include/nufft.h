@@ -78,7 +78,8 @@ typedef struct {
                         * need T_d = 16 - w); 4 / 8 = smem z-plane owners, that many warps;               *
                         * ablation only (complex transforms; real ones use 8): -1 = the paper's Atomic    *
                         * Spread, one thread per point in caller order, global atomics;*
-                        * -2 = the same over the bin-sorted points                                        */
+                        * -2 = the same over the bin-sorted points; -3 = the paper's Tiled Spread       *
+                        * (PAPER.md:203-206): shared-memory histogram, shared atomics, 4 z-slice teams/bin */
     int precompute;    /* ES weights of every point (3 w reals, sorted order) computed once by setpts and
                         * read by every execute / spread / interp instead of re-evaluating phi:
                         * 0 = auto (widths w >= 6, when the table fits in 1/4 of the device memory),
@@ -86,8 +87,14 @@ typedef struct {
     int interp_method; /* 0 = tiled (subgrid staged in shared memory, default); ablation only (complex *
                         * type 2 / nufft_interp): 1 = the paper's Direct Interpolation, one thread per    *
                         * point in caller order reading global memory; 2 = the same   *
-                        * over the bin-sorted points                                   */
-    int reserved[4];
+                        * over the bin-sorted points; 3 = the same along the Morton   *
+                        * (Z-order) curve of the bins                                   */
+    int fft_method;    /* fine-grid FFT of the complex transforms (one GPU): 0 = one (2N)^3 cuFFT + mode *
+                        * truncation (default); 1 = the paper's pruned sigma = 2 split (PAPER.md:237-247,  *
+                        * Eq. 7): eight N^3 transforms of the parity sub-grids read / written with stride *
+                        * 2, twiddle combine (type 1) / conjugate-twiddle split (type 2) fused with D;     *
+                        * needs one extra fine-grid-sized buffer.  Slab plans and real transforms: 0 only */
+    int reserved[3];
 } nufft_opts;
 
 typedef struct {

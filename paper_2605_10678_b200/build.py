@@ -31,7 +31,7 @@ CU_FLAGS = ARCH + COMMON + ["--expt-relaxed-constexpr", "-Xptxas", "-v"]
 CU_FLAGS += os.environ.get("NUFFT_EXTRA_NVCC_FLAGS", "").split()
 
 SOURCES = ["sort.cu", "xport.cpp", "spread.cu", "spread_rows.cu", "spread_outer.cu", "spread_sub.cu", "interp.cu", "interp_real.cu", "interp_vec3.cu",
-           "elementwise.cu", "pif.cu", "variants.cu", "spread_tc.cu", "dist_kernels.cu", "peak.cu", "plan.cpp", "dist.cpp"]
+           "elementwise.cu", "pif.cu", "variants.cu", "spread_tc.cu", "pruned.cu", "dist_kernels.cu", "peak.cu", "plan.cpp", "dist.cpp"]
 
 
 def _nccl_dirs():

@@ -123,6 +123,22 @@ cudaError_t launch_interp_direct(const Geom& g, const PtsView<T>& p, int64_t nbi
 template <typename T>
 cudaError_t launch_caller_order(const PtRec<T>* rec, int64_t Np, uint32_t* order,
                                 cudaStream_t s);
+// the Morton (Z-order) walk of the bins for Direct Interpolation (interp_method = 3):
+// order[t] = sorted slot of the t-th point along the curve; key_count / key_off hold
+// morton_keys(g) (+ 1) entries, blocksum scan_blocksum_elems(morton_keys(g)), bin_base nbins
+// the paper's Tiled Spread (spread_warps = -3): shared-memory histogram with shared
+// atomics, kTiledZ z-slice teams per bin
+template <typename T>
+cudaError_t launch_spread_tiled(const Geom& g, const PtsView<T>& p, int64_t nbins,
+                                const typename Cx<T>::type* c, typename Cx<T>::type* grid,
+                                double beta, cudaStream_t s);
+size_t spread_tiled_smem_bytes(const Geom& g, int cell_bytes);
+size_t morton_keys(const Geom& g);
+cudaError_t launch_morton_order(const Geom& g, const uint32_t* offset, int64_t nbins, int64_t Np,
+                                uint32_t* key_count, uint32_t* key_off, uint32_t* blocksum,
+                                uint32_t* bin_base, uint32_t* order, cudaStream_t s);
+cudaError_t launch_exclusive_scan(const uint32_t* count, int64_t n, uint32_t* blocksum,
+                                  uint32_t* out, cudaStream_t s);
 // smem row pitch (cells) of the interp's subgrid for complex cells of cell_bytes
 int interp_tile_pitch(int cell_bytes, int T, int W, bool sub = false);
 template <typename T>
@@ -178,6 +194,18 @@ cudaError_t launch_pad_precorrect(const typename Cx<T>::type* fk, const int64_t 
                                   const T* p1, const T* p2, const T* p3, int modeord,
                                   const int64_t nf[3], typename Cx<T>::type* grid,
                                   cudaStream_t s);
+
+// pruned.cu: the paper's sigma = 2 split FFT (opts.fft_method = 1): S = 8 contiguous
+// N^3 parity-sub-grid spectra (p = px + 2 py + 4 pz) -> retained modes (twiddles, chi,
+// D); and the mirror fk -> 8 pre-corrected, twiddled sub-spectra H
+template <typename T>
+cudaError_t launch_pruned_combine(const typename Cx<T>::type* S, const int64_t N[3], const T* p1,
+                                  const T* p2, const T* p3, int modeord, int sign,
+                                  typename Cx<T>::type* fk, cudaStream_t st);
+template <typename T>
+cudaError_t launch_pruned_split(const typename Cx<T>::type* fk, const int64_t N[3], const T* p1,
+                                const T* p2, const T* p3, int modeord, int sign,
+                                typename Cx<T>::type* H, cudaStream_t st);
 
 // real-valued transforms: R2C half spectrum H (nf3 x nf2 x (nf1/2 + 1), x fastest)
 template <typename T>

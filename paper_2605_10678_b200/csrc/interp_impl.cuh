@@ -400,18 +400,13 @@ __device__ __forceinline__ void row_sums(const Cell (&blk)[NCOMP][2][kBlk], cons
 #pragma unroll
     for (int m = 0; m < NC; ++m) {
         const int q = NCOMP == 1 ? 0 : m, cm = NCOMP == 1 ? m : 0;
-        // two interleaved partial sums per row: half the dependent-FMA depth
-        T s0a = 0, s0b = 0, s1a = 0, s1b = 0;
+        T s0 = 0, s1 = 0;
 #pragma unroll
-        for (int k = 0; k < W; k += 2) {
-            s0a = fma(CellGet<Cell>::get(blk[q][0][D + k], cm), wx[k], s0a);
-            s1a = fma(CellGet<Cell>::get(blk[q][1][D + k], cm), wx[k], s1a);
-            if (k + 1 < W) {
-                s0b = fma(CellGet<Cell>::get(blk[q][0][D + k + 1], cm), wx[k + 1], s0b);
-                s1b = fma(CellGet<Cell>::get(blk[q][1][D + k + 1], cm), wx[k + 1], s1b);
-            }
+        for (int k = 0; k < W; ++k) {
+            s0 = fma(CellGet<Cell>::get(blk[q][0][D + k], cm), wx[k], s0);
+            s1 = fma(CellGet<Cell>::get(blk[q][1][D + k], cm), wx[k], s1);
         }
-        val[m] = fma(s0a + s0b, f0, (s1a + s1b) * f1);
+        val[m] = fma(s0, f0, s1 * f1);
     }
 }
 // Every point of the current run, grouped by x base D (compile-time register
@@ -425,26 +420,23 @@ __device__ __forceinline__ void run_gather(const Cell (&blk)[NCOMP][2][kBlk],
     if constexpr (D < G) {
         unsigned msk = dmask[D] & run;
         while (msk) {
-            // four points per group, branch-free: an absent slot repeats the first point
-            // with zero weights, so the four row-sum chains interleave
             int jj[4];
-            const int jfirst = __ffs(msk) - 1;
+            T acc[NC][4];
 #pragma unroll
             for (int g4 = 0; g4 < 4; ++g4) {
                 jj[g4] = msk ? __ffs(msk) - 1 : -1;
                 msk &= msk - 1;
-            }
-            T acc[NC][4];
 #pragma unroll
-            for (int g4 = 0; g4 < 4; ++g4) {
-                const bool ok = jj[g4] >= 0;
-                const int j = ok ? jj[g4] : jfirst;
-                const T wyv = ok ? swy[j * kYS + ry] : (T)0;
-                const T f0 = wyv * swz[j * kYS + rz], f1 = wyv * swz[j * kYS + rz + 4];
-                T val[NC];
-                row_sums<T, Cell, NCOMP, NC, W, D>(blk, swx + j * W, f0, f1, val);
+                for (int m = 0; m < NC; ++m) acc[m][g4] = 0;
+                if (jj[g4] >= 0) {
+                    const int j = jj[g4];
+                    const T wyv = swy[j * kYS + ry];
+                    const T f0 = wyv * swz[j * kYS + rz], f1 = wyv * swz[j * kYS + rz + 4];
+                    T val[NC];
+                    row_sums<T, Cell, NCOMP, NC, W, D>(blk, swx + j * W, f0, f1, val);
 #pragma unroll
-                for (int m = 0; m < NC; ++m) acc[m][g4] = val[m];
+                    for (int m = 0; m < NC; ++m) acc[m][g4] = val[m];
+                }
             }
             T tot[NC];
 #pragma unroll

@@ -228,6 +228,7 @@ int local_sort(nufft_plan_s* p, int64_t Np, const void* xd, const void* yd, cons
                                         static_cast<PtRec<float>*>(p->rec), p->nbins, p->stream));
     p->Np = Np;
     p->order_ok = false;
+    p->morton_ok = false;
     // per-point ES weights, reused by every execute on these points
     p->wts_on = false;
     // auto (0): widths w >= 6 (B200, scripts/gpu_precompute.sh, step ms table / in-kernel
@@ -295,6 +296,17 @@ static int caller_order(nufft_plan_s* p, const uint32_t** out) {
 
 int do_spread(nufft_plan_s* p, const void* c_dev, void* grid0) {
     StageTimer tm(p, EV_SPREAD);
+    if (p->geom.spread_warps == -3) {  // the paper's Tiled Spread (shared atomics)
+        if (p->prec == NUFFT_F64)
+            NUFFT_CK(launch_spread_tiled<double>(p->geom, pts_view<double>(p), p->nbins,
+                                                 static_cast<const double2*>(c_dev),
+                                                 static_cast<double2*>(grid0), p->beta, p->stream));
+        else
+            NUFFT_CK(launch_spread_tiled<float>(p->geom, pts_view<float>(p), p->nbins,
+                                                static_cast<const float2*>(c_dev),
+                                                static_cast<float2*>(grid0), p->beta, p->stream));
+        return NUFFT_OK;
+    }
     if (p->geom.spread_warps < 0) {  // Atomic Spread (-1 caller order, -2 bin-sorted)
         const uint32_t* order = nullptr;
         if (p->geom.spread_warps == -1) {
@@ -484,12 +496,41 @@ static const void* interp_tmap(nufft_plan_s* p, const void* grid0) {
     return p->tmap;
 }
 
+// Morton walk of the bins (interp_method = 3): order[t] = sorted slot of point t
+static int morton_order(nufft_plan_s* p, const uint32_t** out) {
+    const size_t nk = morton_keys(p->geom);
+    const size_t n_order = (size_t)p->Np, n_blk = scan_blocksum_elems((int64_t)nk);
+    const size_t need = 4 * (n_order + nk + (nk + 1) + n_blk + (size_t)p->nbins) + 64;
+    if (!p->morton_ok) {
+        if (need > p->morton_bytes) {
+            dev_free(p, &p->morton, p->morton_bytes);
+            p->morton_bytes = 0;
+            int st = dev_alloc(p, &p->morton, need);
+            if (st) return st;
+            p->morton_bytes = need;
+        }
+        uint32_t* order = static_cast<uint32_t*>(p->morton);
+        uint32_t* kc = order + n_order;
+        uint32_t* ko = kc + nk;
+        uint32_t* bs = ko + nk + 1;
+        uint32_t* bb = bs + n_blk;
+        NUFFT_CK(launch_morton_order(p->geom, p->offset, p->nbins, p->Np, kc, ko, bs, bb, order,
+                                     p->stream));
+        p->morton_ok = true;
+    }
+    *out = static_cast<const uint32_t*>(p->morton);
+    return NUFFT_OK;
+}
+
 int do_interp(nufft_plan_s* p, const void* grid0, void* c_dev) {
     StageTimer tm(p, EV_INTERP);
-    if (p->interp_method > 0) {  // Direct Interpolation (1 caller order, 2 bin-sorted)
+    if (p->interp_method > 0) {  // Direct Interpolation (1 caller order, 2 bin-sorted, 3 Morton)
         const uint32_t* order = nullptr;
         if (p->interp_method == 1) {
             int st = caller_order(p, &order);
+            if (st) return st;
+        } else if (p->interp_method == 3) {
+            int st = morton_order(p, &order);
             if (st) return st;
         }
         if (p->prec == NUFFT_F64)
@@ -574,6 +615,113 @@ int do_fft(nufft_plan_s* p, int sign) {
     return r == CUFFT_SUCCESS ? NUFFT_OK : NUFFT_ERR_CUFFT;
 }
 
+// The paper's pruned sigma = 2 FFT (pruned.cu): two strided cuFFT N^3 plans and the
+// buffer of the eight parity-sub-grid spectra, created on first use.
+int ensure_pruned(nufft_plan_s* p) {
+    if (p->fft_sub_ok) return NUFFT_OK;
+    const int64_t nm = p->N[0] * p->N[1] * p->N[2];
+    const size_t need = (size_t)(8 * nm) * p->cplx_size;
+    if (p->fft_aux_bytes < need) {
+        dev_free(p, &p->fft_aux, p->fft_aux_bytes);
+    dev_free(p, &p->morton, p->morton_bytes);
+        p->fft_aux_bytes = 0;
+        int st = dev_alloc(p, &p->fft_aux, need);
+        if (st) return st;
+        p->fft_aux_bytes = need;
+    }
+    int n[3] = {(int)p->N[2], (int)p->N[1], (int)p->N[0]};
+    // sub-grid element (z, y, x) of parity p sits at fine index 2 (x + nf1 (y + nf2 z)) + off(p)
+    int strided[3] = {(int)p->N[2], (int)p->nf[1], (int)p->nf[0]};
+    const cufftType ty = p->prec == NUFFT_F64 ? CUFFT_Z2Z : CUFFT_C2C;
+    if (cufftPlanMany(&p->fft_sub1, 3, n, strided, 2, 1, n, 1, (int)nm, ty, 1) != CUFFT_SUCCESS)
+        return NUFFT_ERR_CUFFT;
+    if (cufftPlanMany(&p->fft_sub2, 3, n, n, 1, (int)nm, strided, 2, 1, ty, 1) != CUFFT_SUCCESS) {
+        cufftDestroy(p->fft_sub1);
+        return NUFFT_ERR_CUFFT;
+    }
+    p->fft_sub_ok = true;
+    size_t w1 = 0, w2 = 0;
+    cufftGetSize(p->fft_sub1, &w1);
+    cufftGetSize(p->fft_sub2, &w2);
+    p->bytes += w1 + w2;
+    if (cufftSetStream(p->fft_sub1, p->stream) != CUFFT_SUCCESS ||
+        cufftSetStream(p->fft_sub2, p->stream) != CUFFT_SUCCESS)
+        return NUFFT_ERR_CUFFT;
+    return NUFFT_OK;
+}
+
+// fine-grid offset of parity sub-grid q = px + 2 py + 4 pz
+size_t parity_offset(const nufft_plan_s* p, int q) {
+    return (size_t)((q & 1) + ((q >> 1) & 1) * p->nf[0] + ((q >> 2) & 1) * p->nf[0] * p->nf[1]);
+}
+
+int sub_fft(nufft_plan_s* p, cufftHandle h, void* in, void* out, int sign) {
+    const int dir = sign < 0 ? CUFFT_FORWARD : CUFFT_INVERSE;
+    cufftResult r;
+    if (p->prec == NUFFT_F64)
+        r = cufftExecZ2Z(h, static_cast<cufftDoubleComplex*>(in),
+                         static_cast<cufftDoubleComplex*>(out), dir);
+    else
+        r = cufftExecC2C(h, static_cast<cufftComplex*>(in), static_cast<cufftComplex*>(out), dir);
+    return r == CUFFT_SUCCESS ? NUFFT_OK : NUFFT_ERR_CUFFT;
+}
+
+// type 1 after the spread: eight strided N^3 FFTs of the fine grid's parity sub-grids,
+// then twiddle combine + truncation + deconvolution
+int pruned_type1(nufft_plan_s* p, void* fkd) {
+    int st = ensure_pruned(p);
+    if (st) return st;
+    const int64_t nm = p->N[0] * p->N[1] * p->N[2];
+    {
+        StageTimer tm(p, EV_FFT);
+        for (int q = 0; q < 8; ++q) {
+            char* in = static_cast<char*>(p->d_grid) + parity_offset(p, q) * p->cplx_size;
+            char* out = static_cast<char*>(p->fft_aux) + (size_t)(q * nm) * p->cplx_size;
+            if ((st = sub_fft(p, p->fft_sub1, in, out, p->iflag))) return st;
+        }
+    }
+    StageTimer tm(p, EV_DECONV);
+    if (p->prec == NUFFT_F64)
+        NUFFT_CK(launch_pruned_combine<double>(
+            static_cast<const double2*>(p->fft_aux), p->N, static_cast<const double*>(p->d_p[0]),
+            static_cast<const double*>(p->d_p[1]), static_cast<const double*>(p->d_p[2]),
+            p->modeord, p->iflag, static_cast<double2*>(fkd), p->stream));
+    else
+        NUFFT_CK(launch_pruned_combine<float>(
+            static_cast<const float2*>(p->fft_aux), p->N, static_cast<const float*>(p->d_p[0]),
+            static_cast<const float*>(p->d_p[1]), static_cast<const float*>(p->d_p[2]),
+            p->modeord, p->iflag, static_cast<float2*>(fkd), p->stream));
+    return NUFFT_OK;
+}
+
+// type 2 before the interp: D + conjugate twiddles into eight N^3 sub-spectra, then
+// eight inverse N^3 FFTs writing the fine grid's parity sub-grids (stride 2)
+int pruned_type2(nufft_plan_s* p, const void* fkd) {
+    int st = ensure_pruned(p);
+    if (st) return st;
+    const int64_t nm = p->N[0] * p->N[1] * p->N[2];
+    {
+        StageTimer tm(p, EV_PAD);
+        if (p->prec == NUFFT_F64)
+            NUFFT_CK(launch_pruned_split<double>(
+                static_cast<const double2*>(fkd), p->N, static_cast<const double*>(p->d_p[0]),
+                static_cast<const double*>(p->d_p[1]), static_cast<const double*>(p->d_p[2]),
+                p->modeord, -p->iflag, static_cast<double2*>(p->fft_aux), p->stream));
+        else
+            NUFFT_CK(launch_pruned_split<float>(
+                static_cast<const float2*>(fkd), p->N, static_cast<const float*>(p->d_p[0]),
+                static_cast<const float*>(p->d_p[1]), static_cast<const float*>(p->d_p[2]),
+                p->modeord, -p->iflag, static_cast<float2*>(p->fft_aux), p->stream));
+    }
+    StageTimer tm(p, EV_FFT);
+    for (int q = 0; q < 8; ++q) {
+        char* in = static_cast<char*>(p->fft_aux) + (size_t)(q * nm) * p->cplx_size;
+        char* out = static_cast<char*>(p->d_grid) + parity_offset(p, q) * p->cplx_size;
+        if ((st = sub_fft(p, p->fft_sub2, in, out, -p->iflag))) return st;
+    }
+    return NUFFT_OK;
+}
+
 int64_t user_np(nufft_plan_s* p) { return p->dist ? dist_user_np(p) : p->Np; }
 
 // bytes of one complex fine grid nf1 nf2 nf3 (the caller's grid of nufft_spread /
@@ -621,9 +769,11 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
     if (!(o.L > 0) || (o.modeord != 0 && o.modeord != 1)) return NUFFT_ERR_ARG;
     if (o.spread_warps != 0 && o.spread_warps != 1 && o.spread_warps != 2 &&
         o.spread_warps != 3 && o.spread_warps != 4 && o.spread_warps != 5 && o.spread_warps != 8 &&
-        o.spread_warps != -1 && o.spread_warps != -2)
+        o.spread_warps != -1 && o.spread_warps != -2 && o.spread_warps != -3)
         return NUFFT_ERR_ARG;
-    if (o.interp_method < 0 || o.interp_method > 2) return NUFFT_ERR_ARG;
+    if (o.interp_method < 0 || o.interp_method > 3) return NUFFT_ERR_ARG;
+    if (o.fft_method < 0 || o.fft_method > 1 || (o.fft_method == 1 && o.comm))
+        return o.fft_method == 1 && o.comm ? NUFFT_ERR_UNSUPPORTED : NUFFT_ERR_ARG;
 
     nufft_plan_s* p = new (std::nothrow) nufft_plan_s();
     if (!p) return NUFFT_ERR_ALLOC;
@@ -652,11 +802,19 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
     }
     p->precompute = o.precompute;
     p->interp_method = o.interp_method;
+    p->fft_method = o.fft_method;
 
     Geom& g = p->geom;
     g.nsub = 1;
     g.G = 0;
-    const bool sub = o.spread_warps == 5;  // sub-bin register-row spread (spread_sub.cu)
+    // sub-bin register-row spread (spread_sub.cu): opts.spread_warps = 5, and the
+    // default for fp64 at w <= 6 (C3e4 / C4 on B200: spread 51.9 -> 18.5 ms, 416 -> 155 ms)
+    // (a caller's tile that is not a whole number of sub-bins keeps the other kernels)
+    bool sub_tiles = true;
+    for (int d = 0; d < 3; ++d)
+        if (o.tile[d] > 0 && (o.tile[d] + 1) % (9 - p->w) != 0) sub_tiles = false;
+    const bool sub = o.spread_warps == 5 || (o.spread_warps == 0 && precision == NUFFT_F64 &&
+                                             spread_sub_width(p->w) && sub_tiles);
     if (sub && !spread_sub_width(p->w)) {
         delete p;
         return NUFFT_ERR_UNSUPPORTED;
@@ -697,7 +855,7 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
     // w <= 12 and T = 16 - w), 4 / 8 = shared-memory z-plane owners with that many
     // warps; 0 = outer products when they apply, else 8 z-plane owners (the
     // fastest on B200 per precision and width, profiles/README.md)
-    g.spread_warps = o.spread_warps;
+    g.spread_warps = sub ? 5 : o.spread_warps;
     if (g.spread_warps == 0) g.spread_warps = spread_outer_applies(g) ? 2 : 8;
     if ((g.spread_warps == 1 && !spread_rows_applies(g)) ||
         (g.spread_warps == 2 && !spread_outer_applies(g)) ||
@@ -842,6 +1000,10 @@ int nufft_execute_type1(nufft_handle p, const void* c, void* fk) {
     if ((st = output_view(p, fk, fk_bytes, &fkd, &staged))) return st;
     NUFFT_CK(cudaMemsetAsync(p->d_grid, 0, cgrid_bytes(p), p->stream));
     if ((st = do_spread(p, cd, p->grid0))) return st;                   // Step 1: C
+    if (p->fft_method == 1) {                                           // Steps 2-4, Eq. (7)
+        if ((st = pruned_type1(p, fkd))) return st;
+        return finish_output(p, fk, fkd, fk_bytes, staged);
+    }
     if ((st = do_fft(p, p->iflag))) return st;                          // Step 2: F
     {
         StageTimer tm(p, EV_DECONV);                                    // Steps 3, 4: chi, D
@@ -875,6 +1037,11 @@ int nufft_execute_type2(nufft_handle p, const void* fk, void* c) {
     void* cd = nullptr;
     bool staged = false;
     if ((st = output_view(p, c, c_bytes, &cd, &staged))) return st;
+    if (p->fft_method == 1) {                                           // D, chi^T, F^-1 (Eq. 7)
+        if ((st = pruned_type2(p, fkd))) return st;
+        if ((st = do_interp(p, p->grid0, cd))) return st;               // C^T
+        return finish_output(p, c, cd, c_bytes, staged);
+    }
     {
         StageTimer tm(p, EV_PAD);                                       // D, chi^T
         if (p->prec == NUFFT_F64)
@@ -1137,6 +1304,12 @@ int nufft_destroy(nufft_handle p) {
     dev_free(p, (void**)&p->count, 0);
     dev_free(p, (void**)&p->offset, 0);
     dev_free(p, (void**)&p->offset_key, 0);
+    if (p->fft_sub_ok) {
+        cufftDestroy(p->fft_sub1);
+        cufftDestroy(p->fft_sub2);
+    }
+    dev_free(p, &p->fft_aux, p->fft_aux_bytes);
+    dev_free(p, &p->morton, p->morton_bytes);
     dev_free(p, (void**)&p->blocksum, 0);
     dev_free(p, (void**)&p->bin_of, 0);
     dev_free(p, (void**)&p->rank_of, 0);

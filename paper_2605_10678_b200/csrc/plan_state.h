@@ -40,6 +40,14 @@ struct nufft_plan_s {
     // real grid is d_grid[0, nf^3) reals, the half spectrum follows it
     cufftHandle fft_r2c = 0, fft_c2r = 0;
     bool fft_r_ok = false;
+    // the paper's pruned sigma = 2 FFT (opts.fft_method = 1, complex transforms): the
+    // eight N^3 parity-sub-grid spectra (fft_aux, = the fine grid's size) and the
+    // strided sub-grid cuFFT plans (type 1: strided in, type 2: strided out)
+    int fft_method = 0;
+    void* fft_aux = nullptr;
+    size_t fft_aux_bytes = 0;
+    cufftHandle fft_sub1 = 0, fft_sub2 = 0;
+    bool fft_sub_ok = false;
     // three real fields, SoA (nufft_execute_type2_real3 / nufft_pif_gather_kick)
     void* vgrid = nullptr;  // = d_grid (grown to 3 fields + half spectrum)
 
@@ -66,6 +74,11 @@ struct nufft_plan_s {
     void* order = nullptr;
     int64_t order_cap = 0;
     bool order_ok = false;
+    // interp_method = 3: the Morton walk of the bins (order | key counts | key offsets |
+    // scan block sums | bin bases, one allocation), rebuilt after each setpts
+    void* morton = nullptr;
+    size_t morton_bytes = 0;
+    bool morton_ok = false;
     // per-point ES weights (opts.precompute): Np x 3w reals in sorted order
     int precompute = 0;     // opts value: 0 auto, 1 always, -1 never
     void* wts = nullptr;

@@ -339,6 +339,18 @@ cudaError_t launch_bin_sort(const Geom& g, int64_t Np, const T* x, const T* y, c
     return cudaGetLastError();
 }
 
+// out = exclusive prefix sum of count[0, n) (n + 1 entries: out[n] = total), the same
+// three-phase warp-shuffle scan as setpts; blocksum: scan_blocksum_elems(n) entries
+cudaError_t launch_exclusive_scan(const uint32_t* count, int64_t n, uint32_t* blocksum,
+                                  uint32_t* out, cudaStream_t s) {
+    const int64_t ntiles = (n + kScanTile - 1) / kScanTile;
+    if (ntiles == 0) return cudaMemsetAsync(out, 0, sizeof(uint32_t), s);
+    scan_tile_sums<<<(unsigned)ntiles, kScanThreads, 0, s>>>(count, n, blocksum);
+    scan_sums<<<1, kScanThreads, 0, s>>>(blocksum, ntiles);
+    scan_tiles<<<(unsigned)ntiles, kScanThreads, 0, s>>>(count, n, blocksum, out);
+    return cudaGetLastError();
+}
+
 template <typename T>
 cudaError_t launch_weights(const PtRec<T>* rec, int64_t Np, int w, double beta, T* out,
                            cudaStream_t s) {

@@ -463,10 +463,13 @@ cudaError_t launch_nw(const Geom& g, const PtsView<T>& p, int64_t nbins, const V
     if (nbins > 0) kern<<<(unsigned)nbins, 32 * NW, smem, s>>>(g, p, c, grid, (T)beta);
     return cudaGetLastError();
 }
+// the block flush: straight to the fine grid (default; spread_subg_kernel) or
+// NUFFT_SUB_TILE=1 through a shared subgrid of the bin with shared atomics
+// (spread_sub_kernel, measured slower: C3e4 25.0 vs 18.5 ms) -- a measurement switch
 inline bool sub_global() {
     static const bool on = [] {
-        const char* e = std::getenv("NUFFT_SUB_GLOBAL");
-        return e && std::atoi(e) == 1;
+        const char* e = std::getenv("NUFFT_SUB_TILE");
+        return !(e && std::atoi(e) == 1);
     }();
     return on;
 }

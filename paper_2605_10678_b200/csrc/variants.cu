@@ -10,11 +10,15 @@
 //
 // Both walk the points either in the caller's order (`order` = the slot of caller
 // point t, so thread t handles caller point t: the paper's unsorted variants) or
-// in bin-sorted order (order == nullptr: "sorted" Atomic / Direct).
+// in bin-sorted order (order == nullptr: "sorted" Atomic / Direct),
+// or -- Direct Interpolation only -- along the Morton (Z-order) curve of the bins
+// (launch_morton_order).
 // They read the setpts records (bin-local stencil base + phase), so the bin of a
 // sorted slot is found by a binary search of the bin offsets.
 #include "device_util.cuh"
 #include "internal.cuh"
+
+#include <algorithm>
 
 namespace nufft {
 
@@ -133,7 +137,191 @@ __global__ void caller_order_kernel(const PtRec<T>* __restrict__ rec, int64_t Np
     if (s < Np) order[rec[s].perm] = (uint32_t)s;
 }
 
+// ---- Tiled Spread: the bin's points accumulated into a
+// shared-memory histogram of the (T + w)^3 subgrid with shared ATOMIC additions,
+// one point per thread; the subgrid is split along z into Z slices ("multiple
+// teams process the same tile but operate on disjoint z-slices of the output"), one
+// CTA (team) per (bin, slice), so the histogram is (T + w)^2 x ceil((T + w) / Z)
+// cells; after the bin each slice row is added to the fine grid with one bulk
+// reduction (UBLKRED).  On sm_100a the fp32 / fp64 shared adds are CAS loops.
+constexpr int kTiledZ = 4;  // z-oversubscription: teams per bin
+
+template <typename T, int W>
+__global__ void __launch_bounds__(kVarThreads)
+    spread_tiled_kernel(Geom g, PtsView<T> p, const typename Cx<T>::type* __restrict__ c,
+                        typename Cx<T>::type* __restrict__ grid, T beta) {
+    using C = typename Cx<T>::type;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int b = blockIdx.x / kTiledZ, zk = blockIdx.x % kTiledZ;
+    const uint32_t beg = p.offset[b], end = p.offset[b + 1];
+    if (beg == end) return;
+    const int bx = b % g.nb[0], by = (b / g.nb[0]) % g.nb[1], bz = b / (g.nb[0] * g.nb[1]);
+    const TileX tx = tile_x<sizeof(C)>(bx, g.T[0], W);
+    const int P = tx.pitch, Ey = g.T[1] + W, Ez = g.T[2] + W;
+    const int S = (Ez + kTiledZ - 1) / kTiledZ, z0 = zk * S, z1 = min(Ez, z0 + S);
+    if (z0 >= z1) return;
+    C* hist = reinterpret_cast<C*>(smem);  // [S][Ey][P]
+    {
+        float4* z4 = reinterpret_cast<float4*>(hist);
+        const int n4 = (int)(((size_t)S * Ey * P * sizeof(C)) / 16);
+        for (int i = threadIdx.x; i < n4; i += kVarThreads) z4[i] = float4{0.f, 0.f, 0.f, 0.f};
+    }
+    __syncthreads();
+    const T two_over_w = (T)2 / (T)W;
+    for (uint32_t s = beg + threadIdx.x; s < end; s += kVarThreads) {
+        const PtRec<T> r = p.rec[s];
+        const int lx = (int)(r.la & 0xff), ly = (int)((r.la >> 8) & 0xff), lz = (int)(r.la >> 16);
+        if (lz + W <= z0 || lz >= z1) continue;  // no stencil plane in this team's slice
+        T wt[3][W];
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+#pragma unroll
+            for (int k = 0; k < W; ++k)
+                wt[d][k] = p.w ? p.w[(size_t)s * (3 * W) + W * d + k]
+                               : es_weight<T>(((T)k - r.d[d]) * two_over_w, beta);
+        const C cv = c[r.perm];
+#pragma unroll 1
+        for (int k = 0; k < W; ++k) {
+            const int z = lz + k;
+            if (z < z0 || z >= z1) continue;
+            const C cz = vscale(cv, wt[2][k]);
+            for (int j = 0; j < W; ++j) {
+                C* row = hist + ((size_t)(z - z0) * Ey + ly + j) * P + tx.shift + lx;
+                const C cy = vscale(cz, wt[1][j]);
+#pragma unroll
+                for (int i = 0; i < W; ++i) atomic_add_v(row + i, vscale(cy, wt[0][i]));
+            }
+        }
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    const int oy = by * g.T[1] - W / 2, oz = bz * g.T[2] - W / 2;
+    const int nfx = (int)g.nf[0], nfy = (int)g.nf[1];
+    int sg[2], ss[2], sn[2];
+    const int nseg = row_segments(tx.gx0, tx.len, nfx, sg, ss, sn);
+    for (int rr = threadIdx.x; rr < (z1 - z0) * Ey; rr += kVarThreads) {
+        const int cz = rr / Ey, cy = rr - cz * Ey;
+        const int gy = wrap1(oy + cy, nfy), gz = z_row(oz + z0 + cz, g);
+        C* grow = grid + (int64_t)nfx * ((int64_t)gz * nfy + gy);
+        const C* trow = hist + (size_t)rr * P;
+        for (int k = 0; k < (gz < -g.hz_lo ? 0 : nseg); ++k)
+            bulk_red_add(reinterpret_cast<T*>(grow + sg[k]), trow + ss[k],
+                         (unsigned)(sn[k] * sizeof(C)));
+    }
+    bulk_commit();
+    bulk_wait_read();
+}
+
+// ---- Morton-ordered walk ("Morton code ordering"): the bins are
+// visited along the Z-order curve of their coordinates (bits interleaved x fastest,
+// coordinates coarsened by `shift` so the key space stays <= 2^24), the points of a
+// bin in its sorted order.  Built from the bin-sorted records without another sort:
+// per-key point counts (an atomic cursor places the bins sharing a coarsened key),
+// an exclusive scan of the keys, then each sorted slot's rank along the curve.
+__device__ __forceinline__ uint32_t spread_bits(uint32_t v) {  // 10 bits -> every 3rd bit
+    v &= 0x3ffu;
+    v = (v | (v << 16)) & 0x030000ffu;
+    v = (v | (v << 8)) & 0x0300f00fu;
+    v = (v | (v << 4)) & 0x030c30c3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+__device__ __forceinline__ uint32_t morton_key(const Geom& g, int b, int shift) {
+    const uint32_t bx = (uint32_t)(b % g.nb[0]) >> shift,
+                   by = (uint32_t)((b / g.nb[0]) % g.nb[1]) >> shift,
+                   bz = (uint32_t)(b / (g.nb[0] * g.nb[1])) >> shift;
+    return spread_bits(bx) | (spread_bits(by) << 1) | (spread_bits(bz) << 2);
+}
+__global__ void morton_bin_count_kernel(Geom g, int nbins, int shift,
+                                        const uint32_t* __restrict__ offset,
+                                        uint32_t* __restrict__ key_count,
+                                        uint32_t* __restrict__ bin_base) {
+    const int b = blockIdx.x * kVarThreads + threadIdx.x;
+    if (b >= nbins) return;
+    const uint32_t n = offset[b + 1] - offset[b];
+    bin_base[b] = n ? atomicAdd(&key_count[morton_key(g, b, shift)], n) : 0u;
+}
+__global__ void morton_slot_kernel(Geom g, int nbins, int shift, int64_t Np,
+                                   const uint32_t* __restrict__ offset,
+                                   const uint32_t* __restrict__ key_off,
+                                   const uint32_t* __restrict__ bin_base,
+                                   uint32_t* __restrict__ order) {
+    const int64_t s = (int64_t)blockIdx.x * kVarThreads + threadIdx.x;
+    if (s >= Np) return;
+    int lo = 0, hi = nbins;  // bin of sorted slot s
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (offset[mid] <= (uint32_t)s) lo = mid;
+        else hi = mid;
+    }
+    order[key_off[morton_key(g, lo, shift)] + bin_base[lo] + ((uint32_t)s - offset[lo])] =
+        (uint32_t)s;
+}
+
 }  // namespace
+
+size_t spread_tiled_smem_bytes(const Geom& g, int cell_bytes) {
+    const int P = cell_bytes == 16 ? tile_pitch<16>(g.T[0], g.w) : tile_pitch<8>(g.T[0], g.w);
+    const int Ez = g.T[2] + g.w, S = (Ez + kTiledZ - 1) / kTiledZ;
+    return (size_t)S * (g.T[1] + g.w) * P * cell_bytes;
+}
+
+template <typename T>
+cudaError_t launch_spread_tiled(const Geom& g, const PtsView<T>& p, int64_t nbins,
+                                const typename Cx<T>::type* c, typename Cx<T>::type* grid,
+                                double beta, cudaStream_t s) {
+    const size_t smem = spread_tiled_smem_bytes(g, (int)sizeof(typename Cx<T>::type));
+    const unsigned nb = (unsigned)(nbins * kTiledZ);
+#define CASE(WW)                                                                             \
+    case WW: {                                                                               \
+        auto kern = spread_tiled_kernel<T, WW>;                                              \
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                             (int)smem);                                     \
+        if (e != cudaSuccess) return e;                                                      \
+        if (nb) kern<<<nb, kVarThreads, smem, s>>>(g, p, c, grid, (T)beta);                  \
+        break;                                                                               \
+    }
+    switch (g.w) {
+        CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11)
+        CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
+        default: return cudaErrorInvalidValue;
+    }
+#undef CASE
+    return cudaGetLastError();
+}
+template cudaError_t launch_spread_tiled<float>(const Geom&, const PtsView<float>&, int64_t,
+                                                const float2*, float2*, double, cudaStream_t);
+template cudaError_t launch_spread_tiled<double>(const Geom&, const PtsView<double>&, int64_t,
+                                                 const double2*, double2*, double, cudaStream_t);
+
+int morton_shift(const Geom& g) {
+    int m = std::max(g.nb[0], std::max(g.nb[1], g.nb[2])), bits = 0;
+    while ((1 << bits) < m) ++bits;
+    return bits > 8 ? bits - 8 : 0;  // 3 x 8 bits: a 2^24-entry key space
+}
+size_t morton_keys(const Geom& g) { return (size_t)1 << (3 * (std::min(8, [&] {
+    int m = std::max(g.nb[0], std::max(g.nb[1], g.nb[2])), bits = 0;
+    while ((1 << bits) < m) ++bits;
+    return bits;
+}()))); }
+
+cudaError_t launch_morton_order(const Geom& g, const uint32_t* offset, int64_t nbins, int64_t Np,
+                                uint32_t* key_count, uint32_t* key_off, uint32_t* blocksum,
+                                uint32_t* bin_base, uint32_t* order, cudaStream_t s) {
+    const int shift = morton_shift(g);
+    const size_t nk = morton_keys(g);
+    cudaError_t e = cudaMemsetAsync(key_count, 0, sizeof(uint32_t) * nk, s);
+    if (e != cudaSuccess) return e;
+    if (nbins > 0)
+        morton_bin_count_kernel<<<(unsigned)((nbins + kVarThreads - 1) / kVarThreads), kVarThreads,
+                                  0, s>>>(g, (int)nbins, shift, offset, key_count, bin_base);
+    if ((e = launch_exclusive_scan(key_count, (int64_t)nk, blocksum, key_off, s)) != cudaSuccess)
+        return e;
+    if (Np > 0)
+        morton_slot_kernel<<<(unsigned)((Np + kVarThreads - 1) / kVarThreads), kVarThreads, 0, s>>>(
+            g, (int)nbins, shift, Np, offset, key_off, bin_base, order);
+    return cudaGetLastError();
+}
 
 template <typename T>
 cudaError_t launch_spread_atomic(const Geom& g, const PtsView<T>& p, int64_t nbins,

@@ -38,7 +38,8 @@ class Opts(ctypes.Structure):
                 ("comm", ctypes.c_void_p), ("points_owned", ctypes.c_int),
                 ("tile", ctypes.c_int * 3), ("timing", ctypes.c_int),
                 ("spread_warps", ctypes.c_int), ("precompute", ctypes.c_int),
-                ("interp_method", ctypes.c_int), ("reserved", ctypes.c_int * 4)]
+                ("interp_method", ctypes.c_int), ("fft_method", ctypes.c_int),
+                ("reserved", ctypes.c_int * 3)]
 
 
 class Info(ctypes.Structure):
@@ -195,11 +196,13 @@ class Plan:
                    in caller / bin-sorted order (ablation only)
     interp_method: 0 tiled (default); 1 / 2 = the paper's Direct Interpolation in
                    caller / bin-sorted order (ablation only)
+    fft_method : 0 one (2N)^3 FFT (default); 1 the paper's pruned sigma = 2 split into
+                 eight N^3 parity sub-grid FFTs (complex transforms, one GPU)
     """
 
     def __init__(self, N, eps, precision="f64", iflag=-1, L=2 * math.pi, modeord=0,
                  device=None, stream=None, tile=None, timing=False, spread_warps=0,
-                 comm=None, points_owned=False, precompute=0, interp_method=0):
+                 comm=None, points_owned=False, precompute=0, interp_method=0, fft_method=0):
         if not torch.cuda.is_available():
             raise NufftError("libnufft requires a CUDA device (no CPU fallback)")
         self.N = tuple(int(n) for n in N)
@@ -219,6 +222,7 @@ class Plan:
         o.spread_warps = int(spread_warps)
         o.precompute = int(precompute)
         o.interp_method = int(interp_method)
+        o.fft_method = int(fft_method)
         if comm is not None:
             o.comm = comm._h
             o.points_owned = 1 if points_owned else 0

@@ -275,11 +275,12 @@ def test_precomputed_weights_both_paths(nb, prec, kernel, precompute):
 
 
 @pytest.mark.parametrize("prec", ["f64", "f32"])
-@pytest.mark.parametrize("variant", [(-1, 1), (-2, 2)])
+@pytest.mark.parametrize("variant", [(-1, 1), (-2, 2), (0, 3), (-3, 0)])
 @pytest.mark.parametrize("precompute", [-1, 1])
 def test_ablation_variants_atomic_spread_direct_interp(nb, prec, variant, precompute):
     # the paper's Atomic Spread / Direct Interpolation,
-    # in caller order (-1 / 1) and bin-sorted order (-2 / 2), clustered points
+    # in caller order (-1 / 1) and bin-sorted order (-2 / 2), Direct Interpolation
+    # along the Morton curve of the bins (3), the Tiled Spread (-3), clustered points
     # included (atomic contention), to the same oracle bars as the default kernels
     sw, im = variant
     eps = 1e-9 if prec == "f64" else 1e-5
@@ -410,3 +411,24 @@ def test_config2_fp32_full_parity(nb):
         sm = rng.choice(np.prod(N), 300, replace=False)
         e1 = err(g1.ravel()[sm], oracle.nudft1(x, y, z, np64(c), N, sel=sm))
         assert e1 <= 10 * eps
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("modeord,iflag", [(0, -1), (1, 1)])
+def test_pruned_sigma2_fft_option(nb, prec, modeord, iflag):
+    # opts.fft_method = 1: the paper's pruned FFT (Eq. 7) -- eight
+    # N^3 parity-sub-grid transforms + twiddle combine / split -- equals the full
+    # (2N)^3 transform + truncation on the same points, and the oracle
+    eps = 1e-9 if prec == "f64" else 1e-5
+    N, Np = (24, 32, 20), 30000
+    pts, c = host_inputs(Np, prec, seed=23)
+    fk = synthetic.modes(*N).to(c.dtype)
+    _, a1, a2 = run_pair(nb, N, eps, prec, pts, c, fk, iflag=iflag, modeord=modeord)
+    _, b1, b2 = run_pair(nb, N, eps, prec, pts, c, fk, iflag=iflag, modeord=modeord, fft_method=1)
+    same = 1e-13 if prec == "f64" else 1e-5
+    assert err(b1, a1) <= same
+    assert err(b2, a2) <= same
+    if modeord == 0:
+        x, y, z = (np64(p) for p in pts)
+        assert err(b1, oracle.type1(x, y, z, np64(c), N, eps, iflag=iflag)) <= TOL[prec]
+        assert err(b2, oracle.type2(x, y, z, np64(fk), eps, iflag=iflag)) <= TOL[prec]
