@@ -18,8 +18,13 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
-BUILD = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "libnufft.so")
+# NUFFT_DEBUG_BOUNDS=1: a separate bounds-checked build (device asserts on every
+# shared-memory / grid index of the hot kernels, NUFFT_CHECK in device_util.cuh) into
+# libnufft_debug.so -- the substitute for compute-sanitizer, which is closed on the
+# GPU pool; select it at run time with NUFFT_LIB=.../libnufft_debug.so
+DEBUG = os.environ.get("NUFFT_DEBUG_BOUNDS") == "1"
+BUILD = os.path.join(HERE, "_build_debug" if DEBUG else "_build")
+LIB = os.path.join(HERE, "libnufft_debug.so" if DEBUG else "libnufft.so")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 
@@ -29,6 +34,8 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler",
 CU_FLAGS = ARCH + COMMON + ["--expt-relaxed-constexpr", "-Xptxas", "-v"]
 # developer instrumentation only (e.g. -DNUFFT_OUTER_PROF); never set for the product build
 CU_FLAGS += os.environ.get("NUFFT_EXTRA_NVCC_FLAGS", "").split()
+if DEBUG:
+    CU_FLAGS += ["-DNUFFT_DEBUG_BOUNDS"]
 
 SOURCES = ["sort.cu", "xport.cpp", "spread.cu", "spread_rows.cu", "spread_outer.cu", "spread_sub.cu", "interp.cu", "interp_real.cu", "interp_vec3.cu",
            "elementwise.cu", "pif.cu", "variants.cu", "spread_tc.cu", "pruned.cu", "dist_kernels.cu", "peak.cu", "plan.cpp", "dist.cpp"]

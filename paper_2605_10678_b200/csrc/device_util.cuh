@@ -6,6 +6,25 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// NUFFT_CHECK(cond): a device-side bounds assertion, compiled only into the
+// bounds-checked build (NUFFT_DEBUG_BOUNDS, build.py); traps the kernel with the
+// failing file / line.  A no-op in the product build.
+#ifdef NUFFT_DEBUG_BOUNDS
+#include <cstdio>
+#define NUFFT_CHECK(cond)                                                              \
+    do {                                                                               \
+        if (!(cond)) {                                                                 \
+            printf("NUFFT_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__,     \
+                   __LINE__, #cond, (int)blockIdx.x, (int)threadIdx.x);                \
+            __trap();                                                                  \
+        }                                                                              \
+    } while (0)
+#else
+#define NUFFT_CHECK(cond) \
+    do {                  \
+    } while (0)
+#endif
+
 namespace nufft {
 namespace dev {
 
@@ -95,6 +114,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
 // ---- 1D bulk copy global -> shared, completion counted on an mbarrier (UBLKCP)
 __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, unsigned bytes,
                                          uint64_t* bar) {
+    NUFFT_CHECK((reinterpret_cast<uintptr_t>(src_gmem) & 15) == 0 && (bytes & 15) == 0 &&
+                (smem_addr(dst_smem) & 15) == 0);
     asm volatile(
         "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
             smem_addr(dst_smem)),
@@ -105,6 +126,8 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, u
 // ---- 1D bulk reduction shared -> global (UBLKRED ... ADD): dst[i] += src[i]
 __device__ __forceinline__ void bulk_red_add(float* dst_gmem, const void* src_smem,
                                              unsigned bytes) {
+    NUFFT_CHECK((reinterpret_cast<uintptr_t>(dst_gmem) & 15) == 0 && (bytes & 15) == 0 &&
+                (smem_addr(src_smem) & 15) == 0);
     asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(
                      dst_gmem),
                  "r"(smem_addr(src_smem)), "r"(bytes)
@@ -112,6 +135,8 @@ __device__ __forceinline__ void bulk_red_add(float* dst_gmem, const void* src_sm
 }
 __device__ __forceinline__ void bulk_red_add(double* dst_gmem, const void* src_smem,
                                              unsigned bytes) {
+    NUFFT_CHECK((reinterpret_cast<uintptr_t>(dst_gmem) & 15) == 0 && (bytes & 15) == 0 &&
+                (smem_addr(src_smem) & 15) == 0);
     asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(
                      dst_gmem),
                  "r"(smem_addr(src_smem)), "r"(bytes)

@@ -541,6 +541,8 @@ __global__ void __launch_bounds__(32 * NW, 1)
             const int sx = lx / G, sy = ly / G, sz = lz / G;
             const int dy = ly - sy * G, dz = lz - sz * G;
             my_dx = lx - sx * G;
+            NUFFT_CHECK(dy + W <= kBlk && dz + W <= kBlk && my_dx + W <= kBlk &&
+                        sz * G + kBlk <= Ez && sy * G + kBlk <= Ey);
             my_sub = sx | (sy << 8) | (sz << 16);
             T wt[3][W];
             if (p.w) {
@@ -588,6 +590,8 @@ __global__ void __launch_bounds__(32 * NW, 1)
                         const Cell* row = tile + q * ncell + (sz * G + rz + 4 * r) * PS +
                                           (sy * G + ry) * P + tx.shift + sx * G;
 #pragma unroll
+                        NUFFT_CHECK(tx.shift + sx * G + kBlk <= P &&
+                                    (sz * G + rz + 4 * r) * PS + (sy * G + ry) * P < ncell);
                         for (int k = 0; k < kBlk; ++k) blk[q][r][k] = row[k];
                     }
             }

@@ -235,7 +235,10 @@ __global__ void __launch_bounds__(kSortThreads) scatter_kernel(
 #pragma unroll
         for (int u = 0; u < kScatterILP; ++u) {
             const int64_t i = i0 + u * stride;
-            if (i < Np) slot[u] = offset[slot[u]] + rank_of[i];
+            if (i < Np) {
+                slot[u] = offset[slot[u]] + rank_of[i];
+                NUFFT_CHECK(slot[u] < (uint32_t)Np);
+            }
         }
 #pragma unroll
         for (int u = 0; u < kScatterILP; ++u) {

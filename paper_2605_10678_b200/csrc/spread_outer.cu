@@ -304,7 +304,10 @@ __global__ void __launch_bounds__(kOutThreads, OuterMinBlocks<T>::value)
 #pragma unroll
     for (int k = 0; k < 4; ++k)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) tile[((z0 + k) * E + y0 + i) * P + tx.shift + x] = acc[k][i];
+        for (int i = 0; i < 4; ++i) {
+            NUFFT_CHECK(tx.shift + x < P);
+            tile[((z0 + k) * E + y0 + i) * P + tx.shift + x] = acc[k][i];
+        }
     if constexpr (P > E) {  // zero the P - E pad columns outside the shifted window
         const int rr = threadIdx.x;  // E*E == kOutThreads rows
 #pragma unroll

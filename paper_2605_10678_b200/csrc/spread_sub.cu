@@ -126,6 +126,7 @@ template <typename V, int G>
 __device__ __forceinline__ void flush_block(V* tile, int sub, int PS, int P, int shift, int ry,
                                             int rz, V (&acc)[2][kBlk]) {
     const int sx = sub & 0xff, sy = (sub >> 8) & 0xff, sz = sub >> 16;
+    NUFFT_CHECK(sz * G + rz + 4 < PS && sy * G + ry < PS / P && shift + sx * G + kBlk <= P);
     const bool flip = rz & 1;
     constexpr int R = Atom<V>::rounds;
 #pragma unroll
@@ -204,6 +205,8 @@ __global__ void __launch_bounds__(32 * NW, 1)
             const int sx = lx / G, sy = ly / G, sz = lz / G;
             const int dy = ly - sy * G, dz = lz - sz * G;
             my_dx = lx - sx * G;
+            NUFFT_CHECK(sx < g.ns[0] && sy < g.ns[1] && sz < g.ns[2] && dy + W <= kBlk &&
+                        dz + W <= kBlk && my_dx + W <= kBlk);
             my_sub = sx | (sy << 8) | (sz << 16);
             const V cv = c[rr.perm];
             T wt[3][W];
@@ -284,7 +287,7 @@ struct SubgSmem {
     static constexpr int FP = A == 1 ? kBlk + 1 : (A == 2 ? kBlk + 2 : kBlk + 4);
     static constexpr size_t stage_bytes =
         ((32 * W * sizeof(V) + 2 * 32 * kYS * sizeof(T)) + 15) / 16 * 16;
-    static constexpr size_t flush_bytes = (size_t)2 * 32 * FP * sizeof(V);
+    static constexpr size_t flush_bytes = (size_t)32 * FP * sizeof(V);  // one row per lane
     static constexpr size_t warp_bytes = stage_bytes + flush_bytes;
     static constexpr size_t bytes() { return kExpTab * sizeof(double) + NW * warp_bytes; }
 };
@@ -304,10 +307,12 @@ __device__ __forceinline__ void flush_global(const Geom& g, V* grid, V* fb, int 
     const int len = A == 1 ? kBlk : ((shift + kBlk + A - 1) / A) * A;
     int sg[2], ss[2], sn[2];
     const int nseg = row_segments(gxw - shift, len, nfx, sg, ss, sn);
-    bulk_wait_read();  // this lane's previous rows have been read by the bulk engine
+    NUFFT_CHECK(shift + kBlk <= FP && sg[0] >= 0 && sg[nseg - 1] + sn[nseg - 1] <= nfx);
+    // one row of the flush buffer per lane: the two rows go one after the other
+    V* row = fb + (size_t)(rz * 8 + ry) * FP;
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
-        V* row = fb + (size_t)(r * 32 + rz * 8 + ry) * FP;
+        bulk_wait_read();  // the bulk engine has read this lane's previous row
         if constexpr (A > 1) {
 #pragma unroll
             for (int k = 0; k < FP; ++k) row[k] = vzero<V>();
@@ -320,24 +325,21 @@ __device__ __forceinline__ void flush_global(const Geom& g, V* grid, V* fb, int 
                 row[k] = acc[r][k];
             acc[r][k] = vzero<V>();
         }
-    }
-    fence_proxy_async_smem();
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
+        fence_proxy_async_smem();
         const int gy = wrap1(oy + sy * G + ry, nfy);
         const int gz = z_row(oz + sz * G + rz + 4 * r, g);
-        if (gz < -g.hz_lo) continue;  // beyond the halo-extended slab: no stencil
-        V* grow = grid + (int64_t)nfx * ((int64_t)gz * nfy + gy);
-        const V* row = fb + (size_t)(r * 32 + rz * 8 + ry) * FP;
-        for (int k = 0; k < nseg; ++k)
-            bulk_red_add(reinterpret_cast<T*>(grow + sg[k]), row + ss[k],
-                         (unsigned)(sn[k] * sizeof(V)));
+        if (gz >= -g.hz_lo) {  // beyond the halo-extended slab: no stencil
+            V* grow = grid + (int64_t)nfx * ((int64_t)gz * nfy + gy);
+            for (int k = 0; k < nseg; ++k)
+                bulk_red_add(reinterpret_cast<T*>(grow + sg[k]), row + ss[k],
+                             (unsigned)(sn[k] * sizeof(V)));
+        }
+        bulk_commit();
     }
-    bulk_commit();
 }
 
 template <typename T, typename V, int W, int NW>
-__global__ void __launch_bounds__(32 * NW, 12 / NW)
+__global__ void __launch_bounds__(32 * NW, 16 / NW)
     spread_subg_kernel(Geom g, PtsView<T> p, const V* __restrict__ c, V* __restrict__ grid,
                        T beta) {
     using S = SubgSmem<T, V, W, NW>;
@@ -381,6 +383,8 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW)
             const int sx = lx / G, sy = ly / G, sz = lz / G;
             const int dy = ly - sy * G, dz = lz - sz * G;
             my_dx = lx - sx * G;
+            NUFFT_CHECK(sx < g.ns[0] && sy < g.ns[1] && sz < g.ns[2] && dy + W <= kBlk &&
+                        dz + W <= kBlk && my_dx + W <= kBlk);
             my_sub = sx | (sy << 8) | (sz << 16);
             const V cv = c[rr.perm];
             T wt[3][W];

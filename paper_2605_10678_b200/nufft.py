@@ -24,7 +24,9 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnufft.so")
+# NUFFT_LIB selects another build of the same library (the bounds-checked
+# libnufft_debug.so of build.py); default: the in-tree product build
+LIB_PATH = os.environ.get("NUFFT_LIB") or os.path.join(_HERE, "libnufft.so")
 
 F32, F64 = 0, 1
 
