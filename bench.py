@@ -497,7 +497,7 @@ def run_pif(args, cfg, comm=None, inner=False):
         comm = nb.Comm() if ws > 1 else None
     sim = LandauPIF(cfg["N"], cfg["Np"], eps=cfg["eps"], dt=cfg["dt"], precision=cfg["prec"],
                     comm=comm, device=device, timing=True, tile=args.tile,
-                    spread_warps=args.spread_warps)
+                    spread_warps=args.spread_warps, fused=getattr(args, 'pif_fused', False))
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=device)
     for _ in range(args.warmup):
         sim.step()
@@ -687,6 +687,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pif", action="store_true", help="skip the PIF s/step key of the c4n line")
+    ap.add_argument("--pif-fused", action="store_true",
+                    help="PIF: one three-field gather with the kick fused (nufft_pif_gather_kick)")
     ap.add_argument("--tile", default=None, help="bin edge T or Tx,Ty,Tz (default: built-in table)")
     ap.add_argument("--spread-warps", type=int, default=0,
                     help="spread kernel: 1 rows, 2 outer products, 4 / 8 smem planes (default: built-in)")

@@ -69,6 +69,34 @@ template <typename T> struct alignas(32) PtRec {
 };
 static_assert(sizeof(PtRec<double>) == 32 && sizeof(PtRec<float>) == 32, "one sector per point");
 
+#ifdef __CUDACC__
+// One record = one 256-bit global access (SASS LDG.E.ENL2.256 / STG.E.ENL2.256 on
+// sm_100a): half the load / store instructions of two 128-bit accesses.
+template <typename T>
+__device__ __forceinline__ PtRec<T> load_rec(const PtRec<T>* p) {
+    union {
+        PtRec<T> r;
+        unsigned long long q[4];
+    } u;
+    asm("ld.global.nc.v4.b64 {%0, %1, %2, %3}, [%4];"
+        : "=l"(u.q[0]), "=l"(u.q[1]), "=l"(u.q[2]), "=l"(u.q[3])
+        : "l"(p));
+    return u.r;
+}
+// streaming store (.cs: written once, read by a later kernel from HBM)
+template <typename T>
+__device__ __forceinline__ void store_rec_cs(PtRec<T>* p, const PtRec<T>& r) {
+    union {
+        PtRec<T> r;
+        unsigned long long q[4];
+    } u;
+    u.r = r;
+    asm volatile("st.global.cs.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(u.q[0]), "l"(u.q[1]),
+                 "l"(u.q[2]), "l"(u.q[3])
+                 : "memory");
+}
+#endif
+
 template <typename T> struct PtsView {
     const uint32_t* offset;  // nbins + 1 bin starts (exclusive scan of counts)
     const uint32_t* offset_sub;  // nbins nsub + 1 sub-bin starts (Geom::nsub > 1), else = offset

@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(kInterpThreads, 2)
         uint32_t my_perm = 0;
         int my_base = 0;
         if (slot < wend) {
-            const PtRec<T> rr = p.rec[slot];
+            const PtRec<T> rr = load_rec(&p.rec[slot]);
             const T d3[3] = {rr.d[0], rr.d[1], rr.d[2]};
             const uint32_t la = rr.la;
             my_perm = rr.perm;
@@ -535,7 +535,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
         const int np = (int)min(32u, wend - c0);
         int my_sub = -1, my_dx = -1;
         if (lane < np) {  // lane: weights of point c0 + lane (overlaps the staging)
-            const PtRec<T> rr = p.rec[c0 + lane];
+            const PtRec<T> rr = load_rec(&p.rec[c0 + lane]);
             const uint32_t la = rr.la;
             const int lx = (int)(la & 0xff), ly = (int)((la >> 8) & 0xff), lz = (int)(la >> 16);
             const int sx = lx / G, sy = ly / G, sz = lz / G;

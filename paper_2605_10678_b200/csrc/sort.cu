@@ -77,39 +77,67 @@ __device__ __forceinline__ double slab_z(const Geom& g, double szg) {
     return sz;
 }
 
+// sort key of one point: bin, or (bin, sub-bin) for sub-bin plans (the scatter's la)
+template <typename T>
+__device__ __forceinline__ uint32_t sort_key(const Geom& g, T xv, T yv, T zv) {
+    const double sx = fold_rescale((double)xv, g.L, g.scale[0], g.nf[0]);
+    const double sy = fold_rescale((double)yv, g.L, g.scale[1], g.nf[1]);
+    const double szg = fold_rescale((double)zv, g.L, g.scale[2], g.nf[2]);
+    const int cx = cell_of(sx, g.nf[0]);
+    const int cy = cell_of(sy, g.nf[1]);
+    int cz = cell_of(szg, g.nf[2]) - (int)g.z_lo;
+    // a slab plan given a point outside its slab (points_owned misuse): keep memory
+    // safe by clamping to the slab (the caller's contract is broken)
+    cz = cz < 0 ? 0 : (cz >= (int)g.nz_loc ? (int)g.nz_loc - 1 : cz);
+    uint32_t bin = (uint32_t)(cx / g.T[0]) +
+                   (uint32_t)g.nb[0] *
+                       ((uint32_t)(cy / g.T[1]) + (uint32_t)g.nb[1] * (uint32_t)(cz / g.T[2]));
+    if (g.nsub > 1) {
+        const double sz = slab_z(g, szg);
+        bin = bin * (uint32_t)g.nsub +
+              sub_of(g, sx, cx, sy, cy, sz, cell_of(sz + (double)g.z_lo, g.nf[2]) - (int)g.z_lo);
+    }
+    return bin;
+}
+
+// kScatterILP points per thread per round, every load issued before any use and the
+// atomics of the round in flight together (the atomic's return -- the rank -- is
+// the latency that bounds this kernel)
 template <typename T>
 __global__ void __launch_bounds__(kSortThreads) bin_count_kernel(
     Geom g, int64_t Np, const T* __restrict__ x, const T* __restrict__ y,
     const T* __restrict__ z, uint32_t* __restrict__ count, uint32_t* __restrict__ bin_of,
     uint32_t* __restrict__ rank_of) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < Np;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        uint32_t bin;
-        {
-            const double sx = fold_rescale((double)x[i], g.L, g.scale[0], g.nf[0]);
-            const double sy = fold_rescale((double)y[i], g.L, g.scale[1], g.nf[1]);
-            const double szg = fold_rescale((double)z[i], g.L, g.scale[2], g.nf[2]);
-            int cx = cell_of(sx, g.nf[0]);
-            int cy = cell_of(sy, g.nf[1]);
-            int cz = cell_of(szg, g.nf[2]) - (int)g.z_lo;
-            // a slab plan given a point outside its slab (points_owned misuse): keep
-            // memory safe by clamping to the slab (the caller's contract is broken)
-            cz = cz < 0 ? 0 : (cz >= (int)g.nz_loc ? (int)g.nz_loc - 1 : cz);
-            bin = (uint32_t)(cx / g.T[0]) +
-                  (uint32_t)g.nb[0] * ((uint32_t)(cy / g.T[1]) + (uint32_t)g.nb[1] * (uint32_t)(cz / g.T[2]));
-            if (g.nsub > 1) {  // sort key = (bin, sub-bin), as the scatter's record
-                const double sz = slab_z(g, szg);
-                bin = bin * (uint32_t)g.nsub +
-                      sub_of(g, sx, cx, sy, cy, sz,
-                             cell_of(sz + (double)g.z_lo, g.nf[2]) - (int)g.z_lo);
-            }
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < Np;
+         i0 += kScatterILP * stride) {
+        T xv[kScatterILP], yv[kScatterILP], zv[kScatterILP];
+#pragma unroll
+        for (int u = 0; u < kScatterILP; ++u) {
+            const int64_t i = i0 + u * stride;
+            const bool ok = i < Np;
+            xv[u] = ok ? x[i] : (T)0;
+            yv[u] = ok ? y[i] : (T)0;
+            zv[u] = ok ? z[i] : (T)0;
         }
+        uint32_t key[kScatterILP], rank[kScatterILP];
+#pragma unroll
+        for (int u = 0; u < kScatterILP; ++u) key[u] = sort_key<T>(g, xv[u], yv[u], zv[u]);
         // one atomicAdd per point: the rank of the point in its bin.  (A warp-
         // aggregated __match_any_sync version was measured slower on B200 for the
         // paper's near-uniform workloads: setpts C2b 0.170 -> 0.152 ms, C3 18.0 ->
         // 16.5 ms without it; collisions inside a warp are rare at ~1e4-1e5 bins.)
-        bin_of[i] = bin;
-        rank_of[i] = atomicAdd(&count[bin], 1u);
+#pragma unroll
+        for (int u = 0; u < kScatterILP; ++u)
+            if (i0 + u * stride < Np) rank[u] = atomicAdd(&count[key[u]], 1u);
+#pragma unroll
+        for (int u = 0; u < kScatterILP; ++u) {
+            const int64_t i = i0 + u * stride;
+            if (i < Np) {
+                bin_of[i] = key[u];
+                rank_of[i] = rank[u];
+            }
+        }
     }
 }
 
@@ -198,18 +226,8 @@ __global__ void __launch_bounds__(kScanThreads) scan_tiles(const uint32_t* __res
     if (blockIdx.x == gridDim.x - 1 && threadIdx.x == blockDim.x - 1) offset[n] = ex;
 }
 
-// one sorted record: two 16-byte streaming stores (.cs: written once, read by
-// the next kernel from HBM; do not keep it in L1)
-template <typename T>
-__device__ __forceinline__ void store_rec_stream(PtRec<T>* dst, const PtRec<T>& r) {
-    const int4* s = reinterpret_cast<const int4*>(&r);
-    int4* d = reinterpret_cast<int4*>(dst);
-    __stcs(d, s[0]);
-    __stcs(d + 1, s[1]);
-}
-
-// slot = offset[bin] + rank; the whole 32-byte record (one full DRAM sector,
-// two 16-byte stores) goes to the slot: the only random access of setpts.
+// slot = offset[bin] + rank; the whole 32-byte record (one full DRAM sector, one
+// 256-bit streaming store) goes to the slot: the only random access of setpts.
 template <typename T>
 __global__ void __launch_bounds__(kSortThreads) scatter_kernel(
     Geom g, int64_t Np, const T* __restrict__ x, const T* __restrict__ y,
@@ -259,7 +277,7 @@ __global__ void __launch_bounds__(kSortThreads) scatter_kernel(
             r.d[2] = (T)ddz;
             r.la = (uint32_t)lax | ((uint32_t)lay << 8) | ((uint32_t)laz << 16);
             r.perm = (uint32_t)i;
-            store_rec_stream(&rec[slot[u]], r);
+            store_rec_cs(&rec[slot[u]], r);
         }
     }
 }

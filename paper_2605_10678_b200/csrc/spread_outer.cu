@@ -137,7 +137,7 @@ __device__ __forceinline__ void produce(int tid, const PtsView<T>& p, const V* _
     group_sync<BAR, NT>();
     OUTER_PROF_T(q1);
     for (int t = tid; t < n; t += NT) {
-        const PtRec<T> r = p.rec[p0 + t];
+        const PtRec<T> r = load_rec(&p.rec[p0 + t]);
         const int la = (int)r.la;
         const int ly = (la >> 8) & 0xff, lz = la >> 16;
         const int yc = ly + W <= 8 ? 0 : (ly >= 8 ? 2 : 1);

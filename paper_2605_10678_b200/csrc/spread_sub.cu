@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
         const int np = (int)min(32u, wend - c0);
         int my_sub = -1, my_dx = -1;
         if (lane < np) {  // lane: weights of point c0 + lane
-            const PtRec<T> rr = p.rec[c0 + lane];
+            const PtRec<T> rr = load_rec(&p.rec[c0 + lane]);
             const uint32_t la = rr.la;
             const int lx = (int)(la & 0xff), ly = (int)((la >> 8) & 0xff), lz = (int)(la >> 16);
             const int sx = lx / G, sy = ly / G, sz = lz / G;
@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW)
         const int np = (int)min(32u, wend - c0);
         int my_sub = -1, my_dx = -1;
         if (lane < np) {
-            const PtRec<T> rr = p.rec[c0 + lane];
+            const PtRec<T> rr = load_rec(&p.rec[c0 + lane]);
             const uint32_t la = rr.la;
             const int lx = (int)(la & 0xff), ly = (int)((la >> 8) & 0xff), lz = (int)(la >> 16);
             const int sx = lx / G, sy = ly / G, sz = lz / G;
