@@ -59,6 +59,9 @@ CONFIGS = {
     # fp64, eps = 1e-4, dt = 0.01; metric = seconds per PIF step
     "c4": dict(name="C4", prec="f64", N=(512, 512, 512), Np=8 * 512 ** 3, eps=1e-4,
                kind="pif", dt=0.01),
+    # the paper's high-accuracy PIF run: eps = 1e-8, dt = 0.003125
+    "c4e8": dict(name="C4-1e-8", prec="f64", N=(512, 512, 512), Np=8 * 512 ** 3, eps=1e-8,
+                 kind="pif", dt=0.003125),
     # small PIF for quick checks
     "pif128": dict(name="PIF-128", prec="f64", N=(128, 128, 128), Np=8 * 128 ** 3, eps=1e-4,
                    kind="pif", dt=0.01),
@@ -72,6 +75,7 @@ def kernels_per_step(info, ws):
     interp; a slab plan adds 2 halo adds and the x/y pack + unpad instead of the
     single-GPU truncate / pad (z_deconv, z_pad take their places)."""
     n = OUR_KERNELS_PER_STEP + (1 if info.get("weights_precomputed") else 0)
+    n += 1 if info.get("sub_bins", 1) > 1 else 0  # sub-bin plans: the per-bin offset gather
     return n + (4 if ws > 1 else 0)
 REF_SAMPLE = 1 << 19
 
@@ -330,6 +334,44 @@ def run_ours(args, cfg):
     ms_per_step = t_max / args.steps
     value = Np_total / (ms_per_step / 1e3)   # all ranks' points per second
 
+    # -- N > 1: setpts WITH redistribution, timed on its own (points handed out round
+    # robin, so (P-1)/P of them move: owner counts, count all-to-all, one host sync,
+    # grouped send / recv of x, y, z, then the local sort) -- PAPER.md:229-235
+    redist = None
+    if ws > 1 and not args.no_redist:
+        del pts
+        torch.cuda.empty_cache()
+        plan_r = nb.Plan(N, cfg["eps"], precision=cfg["prec"], timing=True, device=device,
+                         tile=args.tile, spread_warps=args.spread_warps, comm=comm,
+                         points_owned=False, L=cfg.get("L", 2 * math.pi))
+        import synthetic
+        rdt = torch.float64 if cfg["prec"] == "f64" else torch.float32
+        gen = synthetic.landau_points if cfg["kind"] == "landau" else synthetic.uniform_points
+        allp = gen(Np_total, seed=1, device=device, dtype=rdt)
+        rr = tuple(a[rank::ws].contiguous() for a in allp)
+        del allp
+        torch.cuda.empty_cache()
+        plan_r.setpts(*rr)  # warm-up (allocations)
+        torch.cuda.synchronize()
+        torch.distributed.barrier()
+        nrep = max(2, min(args.steps, 5))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(nrep):
+            plan_r.setpts(*rr)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / nrep], device=device, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        redist = {"ms": float(t.item()), "moved_fraction": (ws - 1) / ws,
+                  "what": "setpts of points handed out round robin (owner counts, NCCL count "
+                          "all-to-all, host sync, grouped send/recv of x, y, z, local sort); "
+                          "max over ranks"}
+        plan_r.close()
+        del rr
+        torch.cuda.empty_cache()
+        pts, _, _ = make_inputs(cfg, rank, ws, device, plan.local_modes())
+
     # -- end to end through the C ABI with pinned host buffers (the device copies of
     # the inputs are released first: the plan stages host arrays in its own buffers)
     def pinned(t):
@@ -424,6 +466,8 @@ def run_ours(args, cfg):
         }
         if pif is not None:
             out["pif"] = pif
+        if redist is not None:
+            out["setpts_redistribute"] = redist
     if ws > 1:
         comm.close()
         torch.distributed.destroy_process_group()
@@ -687,6 +731,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pif", action="store_true", help="skip the PIF s/step key of the c4n line")
+    ap.add_argument("--no-redist", action="store_true",
+                    help="N > 1: skip the setpts-with-redistribution timing")
     ap.add_argument("--pif-fused", action="store_true",
                     help="PIF: one three-field gather with the kick fused (nufft_pif_gather_kick)")
     ap.add_argument("--tile", default=None, help="bin edge T or Tx,Ty,Tz (default: built-in table)")

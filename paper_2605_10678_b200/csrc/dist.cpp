@@ -394,8 +394,8 @@ int dist_init(nufft_plan_s* p) {
     g.hz_hi = d->hhi;
     if (g.T[2] > d->nzl) {
         if (g.nsub > 1) {  // sub-bin plans keep T + 1 = ns G: drop whole sub-bins in z
-            g.ns[2] = std::max(1, (int)((d->nzl + 1) / g.G));
-            g.T[2] = g.ns[2] * g.G - 1;
+            g.ns[2] = std::max(1, (int)((d->nzl + 1) / g.Gs[2]));
+            g.T[2] = g.ns[2] * g.Gs[2] - 1;
             g.nsub = g.ns[0] * g.ns[1] * g.ns[2];
         } else {
             g.T[2] = (int)d->nzl;

@@ -37,13 +37,22 @@ struct Geom {
     int zper;
     int hz_lo, hz_hi;
     // sub-bins (spread_warps = 5): every bin is split into ns[0] x ns[1] x ns[2]
-    // cubes of G stencil-base values per axis (G = 9 - w: a sub-bin's stencils span
-    // 8 cells per axis); setpts sorts by (bin, sub-bin) and keeps the sub-bin
-    // offsets.  nsub = 1, G = 0: no sub-bins
-    int G;
+    // boxes of Gs[d] stencil-base values per axis (sub_common.cuh SubGeom: a sub-bin's
+    // stencils fit one register block); setpts sorts by (bin, sub-bin).  nsub = 1:
+    // no sub-bins
+    int Gs[3];
     int ns[3];
     int nsub;
 };
+
+// Sub-bin extents Gs[3] (stencil bases per sub-bin and axis) of width w: the
+// register block of the sub-bin kernels is 8 x 8 x 4R cells, R = 2 for w <= 6, 3 for
+// w = 7 (sub_common.cuh SubGeom).
+__host__ __device__ inline void sub_extents(int w, int G[3]) {
+    const int R = w <= 6 ? 2 : 3;
+    G[0] = G[1] = 9 - w;
+    G[2] = 4 * R + 1 - w;
+}
 
 // Local z row of a subgrid: periodic wrap on one GPU; on a slab, -1e9 marks a
 // row outside the halo-extended slab (never touched by any stencil).

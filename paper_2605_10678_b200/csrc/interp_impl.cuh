@@ -394,24 +394,24 @@ template <> struct CellGet<float> {
 };
 
 // val[m] = sum_r f_r sum_k blk[q(m)][r][D + k] wx[k] for the x base D (warp-uniform)
-template <typename T, typename Cell, int NCOMP, int NC, int W, int D>
-__device__ __forceinline__ void row_sums(const Cell (&blk)[NCOMP][2][kBlk], const T* wx, T f0,
-                                         T f1, T (&val)[NC]) {
+template <typename T, typename Cell, int NCOMP, int NC, int W, int D, int R>
+__device__ __forceinline__ void row_sums(const Cell (&blk)[NCOMP][R][kBlk], const T* wx,
+                                         const T (&f)[R], T (&val)[NC]) {
 #pragma unroll
     for (int m = 0; m < NC; ++m) {
         const int q = NCOMP == 1 ? 0 : m, cm = NCOMP == 1 ? m : 0;
-        T s0 = 0, s1 = 0;
+        T v = 0;
 #pragma unroll
-        for (int k = 0; k < W; ++k) {
-            s0 = fma(CellGet<Cell>::get(blk[q][0][D + k], cm), wx[k], s0);
-            s1 = fma(CellGet<Cell>::get(blk[q][1][D + k], cm), wx[k], s1);
+        for (int r = 0; r < R; ++r) {
+            T sr = 0;
+#pragma unroll
+            for (int k = 0; k < W; ++k) sr = fma(CellGet<Cell>::get(blk[q][r][D + k], cm), wx[k], sr);
+            v = fma(sr, f[r], v);
         }
-        val[m] = fma(s0, f0, s1 * f1);
+        val[m] = v;
     }
 }
-// Every point of the current run, grouped by x base D (compile-time register
-// indices, no per-point branch), four points at a time: lane partials -> reduce4 ->
-// the caller-order output.
+
 template <typename T, typename Cell, int NCOMP, int NC, int W, int G, int D, typename Out>
 __device__ __forceinline__ void run_gather(const Cell (&blk)[NCOMP][2][kBlk],
                                            const unsigned (&dmask)[G], unsigned run, const T* swx,
@@ -431,9 +431,9 @@ __device__ __forceinline__ void run_gather(const Cell (&blk)[NCOMP][2][kBlk],
                 if (jj[g4] >= 0) {
                     const int j = jj[g4];
                     const T wyv = swy[j * kYS + ry];
-                    const T f0 = wyv * swz[j * kYS + rz], f1 = wyv * swz[j * kYS + rz + 4];
+                    const T f[2] = {wyv * swz[j * kYS + rz], wyv * swz[j * kYS + rz + 4]};
                     T val[NC];
-                    row_sums<T, Cell, NCOMP, NC, W, D>(blk, swx + j * W, f0, f1, val);
+                    row_sums<T, Cell, NCOMP, NC, W, D, 2>(blk, swx + j * W, f, val);
 #pragma unroll
                     for (int m = 0; m < NC; ++m) acc[m][g4] = val[m];
                 }
@@ -463,7 +463,8 @@ __global__ void __launch_bounds__(32 * NW, 1)
     constexpr int NT = 32 * NW;
     extern __shared__ __align__(1024) unsigned char smem[];  // TMA tensor destination
 
-    const int b = blockIdx.x;
+    const int b = super_bin(g.nb, blockIdx.x);
+    if (b < 0) return;
     const uint32_t beg = p.offset[b], end = p.offset[b + 1];
     if (beg == end) return;
 
@@ -612,6 +613,249 @@ size_t sub_smem_nw(const Geom& g) {
     return InterpSubSmem<T, V, W, NW>::bytes((size_t)P * (g.T[1] + W) * (g.T[2] + W));
 }
 
+// ---------------------------------------------------------------------------
+// Sub-bin interpolation WITHOUT a staged subgrid (the default for sub-bin plans):
+// each warp loads the current sub-bin's 8^3 block straight from the fine grid in
+// HBM / L2 into registers (2 rows x 8 cells per lane, periodic wrap per cell) --
+// no (T + w)^3 shared tile, so 16 warps per SM at 128 registers -- and the lanes'
+// partial sums go through a small shared buffer instead of a shuffle butterfly:
+// every point's 32 lane partials are stored in one slot of red[8][32] (swizzled,
+// conflict-free both ways) and every 8 points lane l sums 8 partials of slot l / 4,
+// two xor-shuffles finish the slot.  ~5 instructions of reduction per point instead
+// of ~20.
+template <typename T, typename V, int W, int NW>
+struct InterpSubgSmem {
+    static constexpr int NC = VT<V>::n;
+    // per warp: wx [32][W] | wy, wz zero-padded [32][kYS] | perm [32] | slot point [8] |
+    // red [8][32][NC]
+    static constexpr size_t stage_bytes =
+        ((32 * W + 32 * (kYS + SubGeom<W>::ZS)) * sizeof(T) + 32 * sizeof(int) +
+         8 * sizeof(int) + 15) / 16 * 16;
+    static constexpr size_t red_bytes = (8 * 32 * NC * sizeof(T) + 15) / 16 * 16;
+    static constexpr size_t warp_bytes = stage_bytes + red_bytes;
+    static constexpr size_t bytes() { return kExpTab * sizeof(double) + NW * warp_bytes; }
+};
+
+// column of lane k's partial in slot j: a bijection in k; conflict-free for the
+// stores (slot j, lanes 8q .. 8q + 7) and for the reads (lanes 4 js + q, k = 8 q + i)
+__device__ __forceinline__ int red_col(int j, int k) {
+    return (k & ~7) | ((k & 7) ^ ((2 * (k >> 3) + (j & 1)) & 7));
+}
+
+// sum the n (<= 8) filled slots and hand each total to the output stage
+template <typename T, int NC, typename Out>
+__device__ __forceinline__ void reduce_slots(const T* red, const int* sj, const uint32_t* sperm,
+                                             int n, int lane, const Out& out) {
+    const int js = lane >> 2, q = lane & 3;
+    T tot[NC];
+#pragma unroll
+    for (int m = 0; m < NC; ++m) tot[m] = 0;
+    if (js < n) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const T* e = red + (size_t)(js * 32 + red_col(js, 8 * q + i)) * NC;
+#pragma unroll
+            for (int m = 0; m < NC; ++m) tot[m] += e[m];
+        }
+    }
+#pragma unroll
+    for (int m = 0; m < NC; ++m) {
+        tot[m] += __shfl_xor_sync(0xffffffffu, tot[m], 1);
+        tot[m] += __shfl_xor_sync(0xffffffffu, tot[m], 2);
+    }
+    if (q == 0 && js < n) out(sperm[sj[js]], tot);
+}
+
+template <typename T, typename Cell, int NCOMP, int NC, int W, int GX, int D, int R, int ZS,
+          typename Out>
+__device__ __forceinline__ void run_gather_slots(const Cell (&blk)[NCOMP][R][kBlk],
+                                                 const unsigned (&dmask)[GX], unsigned run,
+                                                 const T* swx, const T* swy, const T* swz,
+                                                 const uint32_t* sperm, T* red, int* sj, int& cnt,
+                                                 int lane, int ry, int rz, const Out& out) {
+    if constexpr (D < GX) {
+        unsigned msk = dmask[D] & run;
+        // two points per step: both points' shared loads and row-sum chains are
+        // independent, so their latencies overlap (the second slot repeats the first
+        // point when the group has an odd count, and is not stored)
+        while (msk) {
+            const int j0 = __ffs(msk) - 1;
+            msk &= msk - 1;
+            const bool two = msk != 0;
+            const int j1 = two ? __ffs(msk) - 1 : j0;
+            msk &= msk - 1;
+            const T wy0 = swy[j0 * kYS + ry], wy1 = swy[j1 * kYS + ry];
+            T f0[R], f1[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                f0[r] = wy0 * swz[j0 * ZS + rz + 4 * r];
+                f1[r] = wy1 * swz[j1 * ZS + rz + 4 * r];
+            }
+            T v0[NC], v1[NC];
+            row_sums<T, Cell, NCOMP, NC, W, D, R>(blk, swx + j0 * W, f0, v0);
+            row_sums<T, Cell, NCOMP, NC, W, D, R>(blk, swx + j1 * W, f1, v1);
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                if (u == 1 && !two) break;
+                T* e = red + (size_t)(cnt * 32 + red_col(cnt, lane)) * NC;
+#pragma unroll
+                for (int m = 0; m < NC; ++m) e[m] = u ? v1[m] : v0[m];
+                if (lane == 0) sj[cnt] = u ? j1 : j0;
+                if (++cnt == 8) {
+                    __syncwarp();
+                    reduce_slots<T, NC>(red, sj, sperm, 8, lane, out);
+                    cnt = 0;
+                    __syncwarp();
+                }
+            }
+        }
+        run_gather_slots<T, Cell, NCOMP, NC, W, GX, D + 1, R, ZS, Out>(
+            blk, dmask, run, swx, swy, swz, sperm, red, sj, cnt, lane, ry, rz, out);
+    }
+}
+
+// MINW resident warps per SM: 16 (128 registers) for one-block fields, 8 for the
+// three component blocks of the PIF field gather
+template <typename T, typename V, int W, int NW, int MINW, typename Out>
+__global__ void __launch_bounds__(32 * NW, (SubGeom<W>::R == 2 ? MINW : (MINW * 3) / 4) / NW)
+    interp_subg_kernel(Geom g, PtsView<T> p, const typename Layout<V>::Cell* __restrict__ grid,
+                       int64_t gstride, Out out, T beta) {
+    using S = InterpSubgSmem<T, V, W, NW>;
+    using Cell = typename Layout<V>::Cell;
+    constexpr int NCOMP = Layout<V>::comps;
+    constexpr int NC = VT<V>::n;
+    using SG = SubGeom<W>;
+    constexpr int R = SG::R, GX = SG::GX, GY = SG::GY, GZ = SG::GZ, ZS = SG::ZS;
+    constexpr int NT = 32 * NW;
+    extern __shared__ __align__(16) unsigned char smem[];
+
+    const int b = super_bin(g.nb, blockIdx.x);
+    if (b < 0) return;
+    const uint32_t beg = p.offset[b], end = p.offset[b + 1];
+    if (beg == end) return;
+    const int bx = b % g.nb[0], by = (b / g.nb[0]) % g.nb[1], bz = b / (g.nb[0] * g.nb[1]);
+    const int ox = bx * g.T[0] - W / 2, oy = by * g.T[1] - W / 2, oz = bz * g.T[2] - W / 2;
+    const int nfx = (int)g.nf[0], nfy = (int)g.nf[1];
+    double* tab = reinterpret_cast<double*>(smem);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned char* st = smem + kExpTab * sizeof(double) + warp * S::warp_bytes;
+    T* swx = reinterpret_cast<T*>(st);                                // [32][W]
+    T* swy = swx + 32 * W;                                            // [32][kYS]
+    T* swz = swy + 32 * kYS;                                          // [32][ZS]
+    uint32_t* sperm = reinterpret_cast<uint32_t*>(swz + 32 * ZS);     // [32]
+    int* sj = reinterpret_cast<int*>(sperm + 32);                     // [8]
+    T* red = reinterpret_cast<T*>(st + S::stage_bytes);               // [8][32][NC]
+    exp_tab_init(tab, threadIdx.x, NT);
+    __syncthreads();
+
+    const uint32_t n = end - beg;
+    const uint32_t wbeg = beg + (uint32_t)(((uint64_t)n * warp) / NW);
+    const uint32_t wend = beg + (uint32_t)(((uint64_t)n * (warp + 1)) / NW);
+    const int ry = lane & 7, rz = lane >> 3;
+    int cur = -1, cnt = 0;
+    Cell blk[NCOMP][R][kBlk];
+
+    for (uint32_t c0 = wbeg; c0 < wend; c0 += 32) {
+        const int np = (int)min(32u, wend - c0);
+        int my_sub = -1, my_dx = -1;
+        if (lane < np) {
+            const PtRec<T> rr = load_rec(&p.rec[c0 + lane]);
+            const uint32_t la = rr.la;
+            const int lx = (int)(la & 0xff), ly = (int)((la >> 8) & 0xff), lz = (int)(la >> 16);
+            const int sx = lx / GX, sy = ly / GY, sz = lz / GZ;
+            const int dy = ly - sy * GY, dz = lz - sz * GZ;
+            my_dx = lx - sx * GX;
+            my_sub = sx | (sy << 8) | (sz << 16);
+            NUFFT_CHECK(dy + W <= kBlk && dz + W <= SG::BZ && my_dx + W <= kBlk);
+            T wt[3][W];
+            if (p.w) {
+                const T* pw = p.w + (size_t)(c0 + lane) * (3 * W);
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+#pragma unroll
+                    for (int k = 0; k < W; ++k) wt[a][k] = pw[a * W + k];
+            } else {
+                const T dd[3] = {rr.d[0], rr.d[1], rr.d[2]};
+                es_weights3<T, W>(dd, beta, tab, wt);
+            }
+            T* wyl = swy + lane * kYS;
+            T* wzl = swz + lane * ZS;
+#pragma unroll
+            for (int k = 0; k < kBlk; ++k) wyl[k] = (T)0;
+#pragma unroll
+            for (int k = 0; k < SG::BZ; ++k) wzl[k] = (T)0;
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                swx[lane * W + k] = wt[0][k];
+                wyl[dy + k] = wt[1][k];
+                wzl[dz + k] = wt[2][k];
+            }
+            sperm[lane] = rr.perm;
+        }
+        unsigned dmask[GX];
+#pragma unroll
+        for (int d = 0; d < GX; ++d) dmask[d] = __ballot_sync(0xffffffffu, my_dx == d);
+        __syncwarp();
+        for (int j = 0; j < np;) {
+            const int sub = __shfl_sync(0xffffffffu, my_sub, j);
+            if (sub != cur) {  // warp-uniform: the new sub-bin's block from the fine grid
+                cur = sub;
+                const int sx = sub & 0xff, sy = (sub >> 8) & 0xff, sz = sub >> 16;
+                const int gy = wrap1(oy + sy * GY + ry, nfy);
+                int gx[kBlk];
+#pragma unroll
+                for (int k = 0; k < kBlk; ++k) gx[k] = wrap1(ox + sx * GX + k, nfx);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int gz = z_row(oz + sz * GZ + rz + 4 * r, g);
+                    const bool ok = gz >= -g.hz_lo;  // beyond the halo-extended slab: unused
+#pragma unroll
+                    for (int q = 0; q < NCOMP; ++q) {
+                        const Cell* row =
+                            grid + q * gstride + (int64_t)nfx * ((int64_t)(ok ? gz : 0) * nfy + gy);
+#pragma unroll
+                        for (int k = 0; k < kBlk; ++k) blk[q][r][k] = row[gx[k]];
+                    }
+                }
+            }
+            const unsigned run = __ballot_sync(0xffffffffu, my_sub == sub);
+            run_gather_slots<T, Cell, NCOMP, NC, W, GX, 0, R, ZS, Out>(
+                blk, dmask, run, swx, swy, swz, sperm, red, sj, cnt, lane, ry, rz, out);
+            j += __popc(run);
+        }
+        if (cnt) {  // the batch's last, partial group of slots (sperm is per batch)
+            __syncwarp();
+            reduce_slots<T, NC>(red, sj, sperm, cnt, lane, out);
+            cnt = 0;
+        }
+        __syncwarp();
+    }
+}
+
+template <typename T, typename V, int W, int NW, int MINW, typename Out>
+cudaError_t launch_subg(const Geom& g, const PtsView<T>& p, const typename Layout<V>::Cell* grid,
+                        Out c, double beta, cudaStream_t s, int64_t gstride) {
+    const size_t smem = InterpSubgSmem<T, V, W, NW>::bytes();
+    auto kern = interp_subg_kernel<T, V, W, NW, MINW, Out>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return e;
+    }
+    kern<<<(unsigned)super_ctas(g.nb), 32 * NW, smem, s>>>(g, p, grid, gstride, c, (T)beta);
+    return cudaGetLastError();
+}
+
+// the staged-subgrid variant (interp_sub_kernel) instead: NUFFT_SUB_TILE=1
+inline bool interp_sub_tile() {
+    static const bool on = [] {
+        const char* e = std::getenv("NUFFT_SUB_TILE");
+        return e && std::atoi(e) == 1;
+    }();
+    return on;
+}
+
 inline int interp_sub_warps() {
     static const int nw = [] {
         const char* e = std::getenv("NUFFT_SUB_WARPS");
@@ -636,7 +880,7 @@ cudaError_t launch_sub_nw(const Geom& g, const PtsView<T>& p, int64_t nbins,
     std::memset(&map, 0, sizeof(map));
     if (tmap) std::memcpy(&map, tmap, sizeof(map));
     if (nbins > 0)
-        kern<<<(unsigned)nbins, 32 * NW, smem, s>>>(g, p, grid, gstride, c, (T)beta, map,
+        kern<<<(unsigned)super_ctas(g.nb), 32 * NW, smem, s>>>(g, p, grid, gstride, c, (T)beta, map,
                                                     tmap ? 1 : 0);
     return cudaGetLastError();
 }
@@ -658,18 +902,26 @@ template <typename T, typename V, int W, typename Out = StoreOut<V>>
 cudaError_t launch_w(const Geom& g, const PtsView<T>& p, int64_t nbins,
                      const typename Layout<V>::Cell* grid, Out c, double beta, cudaStream_t s,
                      int64_t gstride = 0, const void* tmap = nullptr) {
-    if constexpr (W <= 6) {  // plans sorted by sub-bin: the register-block gather
-        if (g.nsub > 1)
-            // 8 warps (up to 255 registers) for the 3-field block, else the switch
-        {
+    if constexpr (W <= 7) {  // plans sorted by sub-bin: the register-block gather
+        if (g.nsub > 1) {
+            if constexpr (W <= 6) {  // NUFFT_SUB_TILE=1: the staged-subgrid variant
+                if (interp_sub_tile()) {
+                    if constexpr (Layout<V>::comps == 3)
+                        return launch_sub_nw<T, V, W, 8, Out>(g, p, nbins, grid, c, beta, s,
+                                                              gstride, tmap);
+                    else
+                        return interp_sub_warps() == 8
+                                   ? launch_sub_nw<T, V, W, 8, Out>(g, p, nbins, grid, c, beta, s,
+                                                                    gstride, tmap)
+                                   : launch_sub_nw<T, V, W, 16, Out>(g, p, nbins, grid, c, beta,
+                                                                     s, gstride, tmap);
+                }
+            }
+            // default: blocks straight from the fine grid
             if constexpr (Layout<V>::comps == 3)
-                return launch_sub_nw<T, V, W, 8, Out>(g, p, nbins, grid, c, beta, s, gstride, tmap);
+                return launch_subg<T, V, W, 4, 8, Out>(g, p, grid, c, beta, s, gstride);
             else
-                return interp_sub_warps() == 8
-                           ? launch_sub_nw<T, V, W, 8, Out>(g, p, nbins, grid, c, beta, s, gstride,
-                                                            tmap)
-                           : launch_sub_nw<T, V, W, 16, Out>(g, p, nbins, grid, c, beta, s,
-                                                             gstride, tmap);
+                return launch_subg<T, V, W, 4, 16, Out>(g, p, grid, c, beta, s, gstride);
         }
     }
     const size_t smem = smem_w<T, V, W>(g);

@@ -573,14 +573,16 @@ int default_tile(int w, int prec, int64_t nf) {
     return t;
 }
 
-bool spread_sub_width(int w) { return w >= 2 && w <= 6; }
+bool spread_sub_width(int w) { return w >= 2 && w <= 7; }
 
-// Sub-bin spread (spread_warps = 5): G = 9 - w stencil bases per sub-bin and axis
-// (the stencils of a sub-bin span 8 cells: the 8 x 8 register rows of a warp), ns
-// sub-bins per bin axis, T = ns G - 1 (la in [0, T] covers ns G values); ns chosen
-// so that the (T + w)^3 subgrid stays <= 20^3 cells
-int sub_default_tile(int w, int64_t nf) {
-    const int G = 9 - w;
+// Sub-bin kernels (spread_warps = 5): Gs[d] stencil bases per sub-bin and axis
+// (SubGeom in sub_common.cuh: 9 - w, and 6 in z for w = 7), ns sub-bins per bin
+// axis, T = ns G - 1 (la in [0, T] covers ns G values); ns chosen so that the bin
+// edge T + w stays <= 20 cells (points per bin ~ (T + 1)^3)
+int sub_default_tile(int w, int axis, int64_t nf) {
+    int Gs[3];
+    sub_extents(w, Gs);
+    const int G = Gs[axis];
     int ns = 1;
     while ((ns + 1) * G - 1 + w <= 20) ++ns;
     int t = ns * G - 1;
@@ -806,13 +808,15 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
 
     Geom& g = p->geom;
     g.nsub = 1;
-    g.G = 0;
+    g.Gs[0] = g.Gs[1] = g.Gs[2] = 0;
     // sub-bin register-row spread (spread_sub.cu): opts.spread_warps = 5, and the
     // default for fp64 at w <= 6 (C3e4 / C4 on B200: spread 51.9 -> 18.5 ms, 416 -> 155 ms)
     // (a caller's tile that is not a whole number of sub-bins keeps the other kernels)
     bool sub_tiles = true;
+    int Gs[3];
+    sub_extents(p->w, Gs);
     for (int d = 0; d < 3; ++d)
-        if (o.tile[d] > 0 && (o.tile[d] + 1) % (9 - p->w) != 0) sub_tiles = false;
+        if (o.tile[d] > 0 && (o.tile[d] + 1) % Gs[d] != 0) sub_tiles = false;
     const bool sub = o.spread_warps == 5 || (o.spread_warps == 0 && precision == NUFFT_F64 &&
                                              spread_sub_width(p->w) && sub_tiles);
     if (sub && !spread_sub_width(p->w)) {
@@ -822,7 +826,7 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
     for (int d = 0; d < 3; ++d) {
         g.nf[d] = p->nf[d];
         int t = o.tile[d] > 0 ? o.tile[d]
-                : sub         ? sub_default_tile(p->w, p->nf[d])
+                : sub         ? sub_default_tile(p->w, d, p->nf[d])
                               : default_tile(p->w, precision, p->nf[d]);
         if (t < 1 || t > 255 || t + p->w + 2 > p->nf[d]) {
             delete p;
@@ -832,15 +836,15 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
         g.nb[d] = (int)((p->nf[d] + t - 1) / t);
         g.scale[d] = (double)p->nf[d] / o.L;
     }
-    if (sub) {  // bins of ns_d sub-bins of G = 9 - w stencil bases: T_d + 1 = ns_d G
-        g.G = 9 - p->w;
+    if (sub) {  // bins of ns_d sub-bins of Gs_d stencil bases: T_d + 1 = ns_d Gs_d
+        sub_extents(p->w, g.Gs);
         g.nsub = 1;
         for (int d = 0; d < 3; ++d) {
-            if ((g.T[d] + 1) % g.G) {
+            if ((g.T[d] + 1) % g.Gs[d]) {
                 delete p;
                 return NUFFT_ERR_ARG;
             }
-            g.ns[d] = (g.T[d] + 1) / g.G;
+            g.ns[d] = (g.T[d] + 1) / g.Gs[d];
             g.nsub *= g.ns[d];
         }
     }
@@ -899,7 +903,7 @@ int nufft_plan(int64_t N1, int64_t N2, int64_t N3, int iflag, double eps, int pr
                 for (int d = 0; d < 3; ++d) {
                     if (g.ns[d] > 1) {
                         --g.ns[d];
-                        g.T[d] -= g.G;
+                        g.T[d] -= g.Gs[d];
                     }
                     g.nb[d] = (int)((p->nf[d] + g.T[d] - 1) / g.T[d]);
                     g.nsub *= g.ns[d];
@@ -1367,6 +1371,7 @@ int nufft_get_info(nufft_handle p, nufft_info* info) {
     info->ms_interp = ms[EV_INTERP];
     info->ms_comm = ms[EV_COMM];
     info->weights_precomputed = p->wts_on ? 1 : 0;
+    info->sub_bins = p->geom.nsub;
     return NUFFT_OK;
 }
 

@@ -66,7 +66,7 @@ __device__ __forceinline__ uint32_t sub_of(const Geom& g, double sx, int cx, dou
     local_stencil(sx, cx, g.T[0], g.w, &lax, &dd);
     local_stencil(sy, cy, g.T[1], g.w, &lay, &dd);
     local_stencil(sz, cz, g.T[2], g.w, &laz, &dd);
-    return (uint32_t)((laz / g.G * g.ns[1] + lay / g.G) * g.ns[0] + lax / g.G);
+    return (uint32_t)((laz / g.Gs[2] * g.ns[1] + lay / g.Gs[1]) * g.ns[0] + lax / g.Gs[0]);
 }
 
 // slab-local z coordinate exactly as the scatter uses it (clamped into the slab)

@@ -87,25 +87,25 @@ template <> struct Atom<float> {
     __device__ static void add(float* d, float v, bool) { atomicAdd(d, v); }
 };
 
-// acc[r][D + k] += b[k] f_r, k < W: one point whose x base is D
-template <typename V, typename T, int W, int D>
-__device__ __forceinline__ void fma_rows(V (&acc)[2][kBlk], const V* b, T f0, T f1) {
+// acc[r][D + k] += b[k] f_r, k < W, r < R: one point whose x base is D
+template <typename V, typename T, int W, int D, int R>
+__device__ __forceinline__ void fma_rows(V (&acc)[R][kBlk], const V* b, const T (&f)[R]) {
 #pragma unroll
     for (int k = 0; k < W; ++k) {
         const V bk = b[k];
-        vfma(acc[0][D + k], bk, f0);
-        vfma(acc[1][D + k], bk, f1);
+#pragma unroll
+        for (int r = 0; r < R; ++r) vfma(acc[r][D + k], bk, f[r]);
     }
 }
 
-// Every point of the current run, grouped by x base: for D = 0 .. G-1 the points
+// Every point of the current run, grouped by x base: for D = 0 .. GX-1 the points
 // whose bit is set in dmask[D] & run (warp-uniform masks), so the register indices
 // of each group are compile-time constants and no per-point branch is taken.
-template <typename V, typename T, int W, int G, int D>
-__device__ __forceinline__ void run_points(V (&acc)[2][kBlk], const unsigned (&dmask)[G],
+template <typename V, typename T, int W, int GX, int D, int R, int ZS>
+__device__ __forceinline__ void run_points(V (&acc)[R][kBlk], const unsigned (&dmask)[GX],
                                            unsigned run, const V* sb, const T* swy,
                                            const T* swz, int ry, int rz) {
-    if constexpr (D < G) {
+    if constexpr (D < GX) {
         unsigned msk = dmask[D] & run;
         const T* wyp = swy + ry;
         const T* wzp = swz + rz;
@@ -113,10 +113,12 @@ __device__ __forceinline__ void run_points(V (&acc)[2][kBlk], const unsigned (&d
             const int j = __ffs(msk) - 1;
             msk &= msk - 1;
             const T wyv = wyp[j * kYS];
-            const T f0 = wyv * wzp[j * kYS], f1 = wyv * wzp[j * kYS + 4];
-            fma_rows<V, T, W, D>(acc, sb + j * W, f0, f1);
+            T f[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) f[r] = wyv * wzp[j * ZS + 4 * r];
+            fma_rows<V, T, W, D, R>(acc, sb + j * W, f);
         }
-        run_points<V, T, W, G, D + 1>(acc, dmask, run, sb, swy, swz, ry, rz);
+        run_points<V, T, W, GX, D + 1, R, ZS>(acc, dmask, run, sb, swy, swz, ry, rz);
     }
 }
 
@@ -157,7 +159,8 @@ __global__ void __launch_bounds__(32 * NW, 1)
     constexpr int NT = 32 * NW;
     extern __shared__ __align__(16) unsigned char smem[];
 
-    const int b = blockIdx.x;
+    const int b = super_bin(g.nb, blockIdx.x);
+    if (b < 0) return;
     const uint32_t beg = p.offset[b], end = p.offset[b + 1];
     if (beg == end) return;
 
@@ -246,7 +249,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
                 cur = sub;
             }
             const unsigned run = __ballot_sync(0xffffffffu, my_sub == sub);
-            run_points<V, T, W, G, 0>(acc, dmask, run, sb, swy, swz, ry, rz);
+            run_points<V, T, W, G, 0, 2, kYS>(acc, dmask, run, sb, swy, swz, ry, rz);
             j += __popc(run);
         }
         __syncwarp();
@@ -281,37 +284,39 @@ __global__ void __launch_bounds__(32 * NW, 1)
 // the misalignment and zero-pad it (A = 16 / cell bytes).
 template <typename T, typename V, int W, int NW>
 struct SubgSmem {
-    static constexpr int G = kBlk + 1 - W;
+    using SG = SubGeom<W>;
     static constexpr int A = sizeof(V) >= 16 ? 1 : 16 / (int)sizeof(V);
     // flush row pitch (cells): 16-byte aligned rows, consecutive rows in distinct banks
     static constexpr int FP = A == 1 ? kBlk + 1 : (A == 2 ? kBlk + 2 : kBlk + 4);
+    // per warp: b = c wx [32][W] values | wy zero-padded [32][kYS] | wz zero-padded [32][ZS]
     static constexpr size_t stage_bytes =
-        ((32 * W * sizeof(V) + 2 * 32 * kYS * sizeof(T)) + 15) / 16 * 16;
+        ((32 * W * sizeof(V) + 32 * (kYS + SG::ZS) * sizeof(T)) + 15) / 16 * 16;
     static constexpr size_t flush_bytes = (size_t)32 * FP * sizeof(V);  // one row per lane
     static constexpr size_t warp_bytes = stage_bytes + flush_bytes;
     static constexpr size_t bytes() { return kExpTab * sizeof(double) + NW * warp_bytes; }
 };
 
-// this lane's two block rows -> its rows of the warp's flush buffer -> bulk reductions
-// into the periodic fine grid (one or two segments per row)
+// this lane's R block rows -> (one at a time) its row of the warp's flush buffer ->
+// bulk reductions into the periodic fine grid (one or two segments per row)
 template <typename T, typename V, int W, int NW>
 __device__ __forceinline__ void flush_global(const Geom& g, V* grid, V* fb, int sub, int ox,
                                              int oy, int oz, int ry, int rz,
-                                             V (&acc)[2][kBlk]) {
+                                             V (&acc)[SubGeom<W>::R][kBlk]) {
     using S = SubgSmem<T, V, W, NW>;
-    constexpr int G = S::G, A = S::A, FP = S::FP;
+    using SG = SubGeom<W>;
+    constexpr int A = S::A, FP = S::FP;
     const int sx = sub & 0xff, sy = (sub >> 8) & 0xff, sz = sub >> 16;
     const int nfx = (int)g.nf[0], nfy = (int)g.nf[1];
-    const int gxw = wrap1(ox + sx * G, nfx);  // block x origin, wrapped
+    const int gxw = wrap1(ox + sx * SG::GX, nfx);  // block x origin, wrapped
     const int shift = gxw & (A - 1);
     const int len = A == 1 ? kBlk : ((shift + kBlk + A - 1) / A) * A;
     int sg[2], ss[2], sn[2];
     const int nseg = row_segments(gxw - shift, len, nfx, sg, ss, sn);
     NUFFT_CHECK(shift + kBlk <= FP && sg[0] >= 0 && sg[nseg - 1] + sn[nseg - 1] <= nfx);
-    // one row of the flush buffer per lane: the two rows go one after the other
+    const int gy = wrap1(oy + sy * SG::GY + ry, nfy);
     V* row = fb + (size_t)(rz * 8 + ry) * FP;
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
+    for (int r = 0; r < SG::R; ++r) {
         bulk_wait_read();  // the bulk engine has read this lane's previous row
         if constexpr (A > 1) {
 #pragma unroll
@@ -326,8 +331,7 @@ __device__ __forceinline__ void flush_global(const Geom& g, V* grid, V* fb, int 
             acc[r][k] = vzero<V>();
         }
         fence_proxy_async_smem();
-        const int gy = wrap1(oy + sy * G + ry, nfy);
-        const int gz = z_row(oz + sz * G + rz + 4 * r, g);
+        const int gz = z_row(oz + sz * SG::GZ + rz + 4 * r, g);
         if (gz >= -g.hz_lo) {  // beyond the halo-extended slab: no stencil
             V* grow = grid + (int64_t)nfx * ((int64_t)gz * nfy + gy);
             for (int k = 0; k < nseg; ++k)
@@ -338,16 +342,19 @@ __device__ __forceinline__ void flush_global(const Geom& g, V* grid, V* fb, int 
     }
 }
 
+// R = 2 (w <= 6): 16 warps per SM at 128 registers; R = 3 (w = 7): 12 at 168
 template <typename T, typename V, int W, int NW>
-__global__ void __launch_bounds__(32 * NW, 16 / NW)
+__global__ void __launch_bounds__(32 * NW, (SubGeom<W>::R == 2 ? 16 : 12) / NW)
     spread_subg_kernel(Geom g, PtsView<T> p, const V* __restrict__ c, V* __restrict__ grid,
                        T beta) {
     using S = SubgSmem<T, V, W, NW>;
-    constexpr int G = S::G;
+    using SG = SubGeom<W>;
+    constexpr int R = SG::R, GX = SG::GX, GY = SG::GY, GZ = SG::GZ, ZS = SG::ZS;
     constexpr int NT = 32 * NW;
     extern __shared__ __align__(16) unsigned char smem[];
 
-    const int b = blockIdx.x;
+    const int b = super_bin(g.nb, blockIdx.x);
+    if (b < 0) return;
     const uint32_t beg = p.offset[b], end = p.offset[b + 1];
     if (beg == end) return;
     const int bx = b % g.nb[0], by = (b / g.nb[0]) % g.nb[1], bz = b / (g.nb[0] * g.nb[1]);
@@ -355,10 +362,10 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW)
     double* tab = reinterpret_cast<double*>(smem);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned char* st = smem + kExpTab * sizeof(double) + warp * S::warp_bytes;
-    V* sb = reinterpret_cast<V*>(st);                                  // [32][W]
-    T* swy = reinterpret_cast<T*>(sb + 32 * W);                         // [32][kYS]
-    T* swz = swy + 32 * kYS;                                            // [32][kYS]
-    V* fb = reinterpret_cast<V*>(st + S::stage_bytes);                  // [64][FP]
+    V* sb = reinterpret_cast<V*>(st);                    // [32][W]
+    T* swy = reinterpret_cast<T*>(sb + 32 * W);           // [32][kYS]
+    T* swz = swy + 32 * kYS;                              // [32][ZS]
+    V* fb = reinterpret_cast<V*>(st + S::stage_bytes);    // [32][FP]
     exp_tab_init(tab, threadIdx.x, NT);
     __syncthreads();
 
@@ -367,9 +374,9 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW)
     const uint32_t wend = beg + (uint32_t)(((uint64_t)n * (warp + 1)) / NW);
     const int ry = lane & 7, rz = lane >> 3;
     int cur = -1;
-    V acc[2][kBlk];
+    V acc[R][kBlk];
 #pragma unroll
-    for (int r = 0; r < 2; ++r)
+    for (int r = 0; r < R; ++r)
 #pragma unroll
         for (int k = 0; k < kBlk; ++k) acc[r][k] = vzero<V>();
 
@@ -380,12 +387,12 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW)
             const PtRec<T> rr = load_rec(&p.rec[c0 + lane]);
             const uint32_t la = rr.la;
             const int lx = (int)(la & 0xff), ly = (int)((la >> 8) & 0xff), lz = (int)(la >> 16);
-            const int sx = lx / G, sy = ly / G, sz = lz / G;
-            const int dy = ly - sy * G, dz = lz - sz * G;
-            my_dx = lx - sx * G;
-            NUFFT_CHECK(sx < g.ns[0] && sy < g.ns[1] && sz < g.ns[2] && dy + W <= kBlk &&
-                        dz + W <= kBlk && my_dx + W <= kBlk);
+            const int sx = lx / GX, sy = ly / GY, sz = lz / GZ;
+            const int dy = ly - sy * GY, dz = lz - sz * GZ;
+            my_dx = lx - sx * GX;
             my_sub = sx | (sy << 8) | (sz << 16);
+            NUFFT_CHECK(sx < g.ns[0] && sy < g.ns[1] && sz < g.ns[2] && dy + W <= kBlk &&
+                        dz + W <= SG::BZ && my_dx + W <= kBlk);
             const V cv = c[rr.perm];
             T wt[3][W];
             if (p.w) {  // precomputed at setpts (opts.precompute)
@@ -399,12 +406,11 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW)
                 es_weights3<T, W>(dd, beta, tab, wt);
             }
             T* wyl = swy + lane * kYS;
-            T* wzl = swz + lane * kYS;
+            T* wzl = swz + lane * ZS;
 #pragma unroll
-            for (int k = 0; k < kBlk; ++k) {
-                wyl[k] = (T)0;
-                wzl[k] = (T)0;
-            }
+            for (int k = 0; k < kBlk; ++k) wyl[k] = (T)0;
+#pragma unroll
+            for (int k = 0; k < SG::BZ; ++k) wzl[k] = (T)0;
 #pragma unroll
             for (int k = 0; k < W; ++k) {
                 sb[lane * W + k] = vscale(cv, wt[0][k]);
@@ -412,9 +418,9 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW)
                 wzl[dz + k] = wt[2][k];
             }
         }
-        unsigned dmask[G];
+        unsigned dmask[GX];
 #pragma unroll
-        for (int d = 0; d < G; ++d) dmask[d] = __ballot_sync(0xffffffffu, my_dx == d);
+        for (int d = 0; d < GX; ++d) dmask[d] = __ballot_sync(0xffffffffu, my_dx == d);
         __syncwarp();
         for (int j = 0; j < np;) {
             const int sub = __shfl_sync(0xffffffffu, my_sub, j);
@@ -423,7 +429,7 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW)
                 cur = sub;
             }
             const unsigned run = __ballot_sync(0xffffffffu, my_sub == sub);
-            run_points<V, T, W, G, 0>(acc, dmask, run, sb, swy, swz, ry, rz);
+            run_points<V, T, W, GX, 0, R, ZS>(acc, dmask, run, sb, swy, swz, ry, rz);
             j += __popc(run);
         }
         __syncwarp();
@@ -450,7 +456,11 @@ size_t smem_nw(const Geom& g) {
 }
 template <typename T, typename V, int W>
 size_t smem_w(const Geom& g) {
-    return std::max(smem_nw<T, V, W, 8>(g), smem_nw<T, V, W, 16>(g));
+    if constexpr (W <= 6)  // the tile-flush variant exists for R = 2 only
+        return std::max(SubgSmem<T, V, W, 4>::bytes(),
+                        std::max(smem_nw<T, V, W, 8>(g), smem_nw<T, V, W, 16>(g)));
+    else
+        return SubgSmem<T, V, W, 4>::bytes();
 }
 
 template <typename T, typename V, int W, int NW>
@@ -464,7 +474,7 @@ cudaError_t launch_nw(const Geom& g, const PtsView<T>& p, int64_t nbins, const V
         cudaGetLastError();
         return e;
     }
-    if (nbins > 0) kern<<<(unsigned)nbins, 32 * NW, smem, s>>>(g, p, c, grid, (T)beta);
+    if (nbins > 0) kern<<<(unsigned)super_ctas(g.nb), 32 * NW, smem, s>>>(g, p, c, grid, (T)beta);
     return cudaGetLastError();
 }
 // the block flush: straight to the fine grid (default; spread_subg_kernel) or
@@ -489,16 +499,19 @@ cudaError_t launch_g(const Geom& g, const PtsView<T>& p, int64_t nbins, const V*
         cudaGetLastError();
         return e;
     }
-    if (nbins > 0) kern<<<(unsigned)nbins, 32 * NW, smem, s>>>(g, p, c, grid, (T)beta);
+    if (nbins > 0) kern<<<(unsigned)super_ctas(g.nb), 32 * NW, smem, s>>>(g, p, c, grid, (T)beta);
     return cudaGetLastError();
 }
 
 template <typename T, typename V, int W>
 cudaError_t launch_w(const Geom& g, const PtsView<T>& p, int64_t nbins, const V* c, V* grid,
                      double beta, cudaStream_t s) {
-    if (sub_global()) return launch_g<T, V, W, 4>(g, p, nbins, c, grid, beta, s);
-    return sub_warps() == 8 ? launch_nw<T, V, W, 8>(g, p, nbins, c, grid, beta, s)
-                            : launch_nw<T, V, W, 16>(g, p, nbins, c, grid, beta, s);
+    if constexpr (W <= 6) {
+        if (!sub_global())
+            return sub_warps() == 8 ? launch_nw<T, V, W, 8>(g, p, nbins, c, grid, beta, s)
+                                    : launch_nw<T, V, W, 16>(g, p, nbins, c, grid, beta, s);
+    }
+    return launch_g<T, V, W, 4>(g, p, nbins, c, grid, beta, s);
 }
 
 template <typename T, typename V>
@@ -511,6 +524,7 @@ cudaError_t launch_v(const Geom& g, const PtsView<T>& p, int64_t nbins, const V*
         case 4: return launch_w<T, V, 4>(g, p, nbins, c, grid, beta, s);
         case 5: return launch_w<T, V, 5>(g, p, nbins, c, grid, beta, s);
         case 6: return launch_w<T, V, 6>(g, p, nbins, c, grid, beta, s);
+        case 7: return launch_w<T, V, 7>(g, p, nbins, c, grid, beta, s);
         default: return cudaErrorNotSupported;
     }
 }
@@ -518,9 +532,11 @@ cudaError_t launch_v(const Geom& g, const PtsView<T>& p, int64_t nbins, const V*
 }  // namespace
 
 bool spread_sub_applies(const Geom& g) {
-    if (g.w < 2 || g.w > 6 || g.nsub <= 1 || g.G != kBlk + 1 - g.w) return false;
+    if (g.w < 2 || g.w > 7 || g.nsub <= 1) return false;
+    int G[3];
+    sub_extents(g.w, G);
     for (int d = 0; d < 3; ++d)
-        if (g.ns[d] < 1 || g.ns[d] * g.G != g.T[d] + 1) return false;
+        if (g.Gs[d] != G[d] || g.ns[d] < 1 || g.ns[d] * G[d] != g.T[d] + 1) return false;
     return true;
 }
 
@@ -533,6 +549,7 @@ size_t spread_sub_smem_bytes(const Geom& g) {
         case 4: return smem_w<T, C, 4>(g);
         case 5: return smem_w<T, C, 5>(g);
         case 6: return smem_w<T, C, 6>(g);
+        case 7: return smem_w<T, C, 7>(g);
         default: return 0;
     }
 }

@@ -9,8 +9,20 @@
 namespace nufft {
 namespace dev {
 
-constexpr int kBlk = 8;  // register block edge: G + w - 1 cells per axis (G = 9 - w)
+constexpr int kBlk = 8;  // register block edge in x and y: G + w - 1 cells (G = 9 - w)
 constexpr int kYS = 9;   // staging stride of a zero-padded 8-row profile (odd: conflict-free)
+
+// Register block of the sub-bin kernels per width: lane l owns the x-rows (y = l & 7,
+// z = (l >> 3) + 4 r), r < R, of an 8 (x) x 8 (y) x 4R (z) cell block; a sub-bin is
+// the G = block - w + 1 stencil bases per axis whose stencils fit the block.  R = 2
+// for w <= 6 (G = 9 - w per axis), R = 3 for w = 7 (G = 2, 2, 6: 24 bases per
+// sub-bin instead of 8, so a block is flushed / reloaded every ~24 points).
+template <int W> struct SubGeom {
+    static constexpr int R = W <= 6 ? 2 : 3;
+    static constexpr int BZ = 4 * R;
+    static constexpr int GX = kBlk + 1 - W, GY = kBlk + 1 - W, GZ = BZ + 1 - W;
+    static constexpr int ZS = BZ + 1;  // staging stride of the zero-padded z profile (odd)
+};
 
 // shared-memory row pitch of a sub-bin kernel's subgrid (cells): rows start 16-byte
 // aligned (bulk copies / reductions) and the 8 block rows of a quarter- / half-warp
@@ -26,6 +38,28 @@ __host__ __device__ __forceinline__ int sub_pitch(int len) {
     const int q = (len + 3) & ~3;
     return (q & 7) == 4 ? q : q + 4;
 }
+// Super-tiled CTA order of the sub-bin kernels: consecutive CTAs walk 8 x 8 x 8
+// blocks of bins (x fastest inside a block, then the blocks row-major), so the bins
+// resident at once form a compact region whose overlapping halos meet in L2 (the
+// row-major order puts the z-neighbour of a bin nb0 x nb1 bins later).  CTAs past
+// the bin grid (ragged blocks) exit at once.
+constexpr int kSuper = 8;
+inline int64_t super_ctas(const int nb[3]) {
+    int64_t n = 1;
+    for (int d = 0; d < 3; ++d) n *= (nb[d] + kSuper - 1) / kSuper;
+    return n * kSuper * kSuper * kSuper;
+}
+__device__ __forceinline__ int super_bin(const int nb[3], int64_t blk) {
+    const int64_t st = blk / (kSuper * kSuper * kSuper);
+    const int w = (int)(blk % (kSuper * kSuper * kSuper));
+    const int s0 = (nb[0] + kSuper - 1) / kSuper, s1 = (nb[1] + kSuper - 1) / kSuper;
+    const int bx = (int)(st % s0) * kSuper + (w % kSuper);
+    const int by = (int)((st / s0) % s1) * kSuper + (w / kSuper) % kSuper;
+    const int bz = (int)(st / ((int64_t)s0 * s1)) * kSuper + w / (kSuper * kSuper);
+    if (bx >= nb[0] || by >= nb[1] || bz >= nb[2]) return -1;
+    return bx + nb[0] * (by + nb[1] * bz);
+}
+
 // plane stride (cells) for a plane of `cells` = pitch x rows: 16-byte aligned, and for
 // 8 / 4-byte cells odd in 8-byte / 4-byte words modulo 4 so that the block rows of
 // consecutive z fall in different banks (16-byte cells: any stride)

@@ -54,7 +54,7 @@ class Info(ctypes.Structure):
                 ("ms_fold", ctypes.c_float), ("ms_fft", ctypes.c_float),
                 ("ms_deconv", ctypes.c_float), ("ms_pad", ctypes.c_float),
                 ("ms_interp", ctypes.c_float), ("ms_comm", ctypes.c_float),
-                ("weights_precomputed", ctypes.c_int)]
+                ("weights_precomputed", ctypes.c_int), ("sub_bins", ctypes.c_int)]
 
     def as_dict(self):
         d = {}

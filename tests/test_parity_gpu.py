@@ -211,16 +211,17 @@ def test_every_spread_kernel(nb, prec, kernel, eps):
 
 
 @pytest.mark.parametrize("prec", ["f64", "f32"])
-@pytest.mark.parametrize("eps", [1e-1, 1e-2, 1e-3, 1e-4, 1e-5])
+@pytest.mark.parametrize("eps", [1e-1, 1e-2, 1e-3, 1e-4, 1e-5, 1e-6])
 def test_sub_bin_spread_every_width(nb, prec, eps):
-    # spread_warps = 5: sub-bin register rows, w = 2 .. 6, default tile (T + 1 = ns G)
+    # spread_warps = 5: sub-bin register rows, w = 2 .. 7 (w = 7: three rows per lane,
+    # 2 x 2 x 6 sub-bins), default tile (T_d + 1 = ns_d G_d)
     N, Np = (32, 24, 40), 40000
     pts, c = host_inputs(Np, prec, seed=21)
     fk = synthetic.modes(*N).to(c.dtype)
     plan, g1, g2 = run_pair(nb, N, eps, prec, pts, c, fk, spread_warps=5)
     w = plan.info()["w"]
-    G = 9 - w
-    assert all((t + 1) % G == 0 for t in plan.info()["tile"])
+    G = (9 - w, 9 - w, (8 if w <= 6 else 12) + 1 - w)
+    assert all((t + 1) % Gd == 0 for t, Gd in zip(plan.info()["tile"], G))
     x, y, z = (np64(p) for p in pts)
     assert err(g1, oracle.type1(x, y, z, np64(c), N, eps)) <= TOL[prec]
     assert err(g2, oracle.type2(x, y, z, np64(fk), eps)) <= TOL[prec]
@@ -230,12 +231,15 @@ def test_sub_bin_spread_every_width(nb, prec, eps):
 def test_sub_bin_spread_tiles_clusters_precompute(nb, prec):
     # ragged / non-cubic tiles, one-hot bins (every point in one cell), precomputed
     # weights, Landau points on [0, 4 pi)^3 -- all against the oracle's spread
-    eps = 1e-4
     N = (24, 20, 28)
-    G = 9 - nb.Plan((8, 8, 8), eps, precision=prec).info()["w"]
     fk = synthetic.modes(*N)
-    cases = [dict(tile=(G - 1, 2 * G - 1, 3 * G - 1)), dict(precompute=1),
-             dict(tile=(3 * G - 1,) * 3, precompute=-1)]
+    cases = []
+    for eps in (1e-4, 1e-6):  # w = 5 (G = 4, 4, 4) and w = 7 (G = 2, 2, 6)
+        w = nb.Plan((8, 8, 8), eps, precision=prec).info()["w"]
+        G = (9 - w, 9 - w, (8 if w <= 6 else 12) + 1 - w)
+        cases += [dict(eps=eps, tile=(G[0] - 1, 2 * G[1] - 1, G[2] - 1)),
+                  dict(eps=eps, precompute=1),
+                  dict(eps=eps, tile=(3 * G[0] - 1, 3 * G[1] - 1, 2 * G[2] - 1), precompute=-1)]
     for kind in ("uniform", "clustered", "one", "landau"):
         L = 4 * math.pi if kind == "landau" else TWO_PI
         if kind == "one":
@@ -247,12 +251,16 @@ def test_sub_bin_spread_tiles_clusters_precompute(nb, prec):
         pts = tuple(p.to(rdt) for p in pts)
         c = c.to(torch.complex128 if prec == "f64" else torch.complex64)
         x, y, z = (np64(p) for p in pts)
-        o1 = oracle.type1(x, y, z, np64(c), N, eps, L=L)
-        o2 = oracle.type2(x, y, z, np64(fk), eps, L=L)
+        ref = {}
+        for eps in (1e-4, 1e-6):
+            ref[eps] = (oracle.type1(x, y, z, np64(c), N, eps, L=L),
+                        oracle.type2(x, y, z, np64(fk), eps, L=L))
         for kw in cases:
+            kw = dict(kw)
+            eps = kw.pop("eps")
             _, g1, g2 = run_pair(nb, N, eps, prec, pts, c, fk.to(c.dtype), L=L, spread_warps=5, **kw)
-            assert err(g1, o1) <= TOL[prec], (kind, kw)
-            assert err(g2, o2) <= TOL[prec], (kind, kw)
+            assert err(g1, ref[eps][0]) <= TOL[prec], (kind, eps, kw)
+            assert err(g2, ref[eps][1]) <= TOL[prec], (kind, eps, kw)
 
 
 @pytest.mark.parametrize("prec", ["f64", "f32"])
