@@ -113,6 +113,7 @@ typedef struct {
     /* per-stage device milliseconds of the most recent calls (opts.timing = 1), else -1 */
     float ms_setpts, ms_spread, ms_fold, ms_fft, ms_deconv, ms_pad, ms_interp, ms_comm;
     int weights_precomputed; /* 1 if the last setpts stored the per-point ES weights     */
+    int sub_bins;           /* sub-bins per bin (sub-bin sorted plans: spread_warps 5), else 1 */
 } nufft_info;
 
 /* Fills *o with the defaults (L = 2 pi, centered modes, default stream, single GPU). */
