@@ -98,6 +98,27 @@ __device__ __forceinline__ void fma_rows(V (&acc)[R][kBlk], const V* b, const T 
     }
 }
 
+// one staged point in registers: b = c wx (W values) and its R row weights wy wz
+template <typename V, typename T, int W, int R>
+struct PtLoad {
+    V b[W];
+    T f[R];
+    __device__ __forceinline__ void load(int j, const V* sb, const T* wyp, const T* wzp, int zs) {
+#pragma unroll
+        for (int k = 0; k < W; ++k) b[k] = sb[j * W + k];
+        const T wyv = wyp[j * kYS];
+#pragma unroll
+        for (int r = 0; r < R; ++r) f[r] = wyv * wzp[j * zs + 4 * r];
+    }
+    template <int D>
+    __device__ __forceinline__ void apply(V (&acc)[R][kBlk]) const {
+#pragma unroll
+        for (int k = 0; k < W; ++k)
+#pragma unroll
+            for (int r = 0; r < R; ++r) vfma(acc[r][D + k], b[k], f[r]);
+    }
+};
+
 // Every point of the current run, grouped by x base: for D = 0 .. GX-1 the points
 // whose bit is set in dmask[D] & run (warp-uniform masks), so the register indices
 // of each group are compile-time constants and no per-point branch is taken.
@@ -109,14 +130,27 @@ __device__ __forceinline__ void run_points(V (&acc)[R][kBlk], const unsigned (&d
         unsigned msk = dmask[D] & run;
         const T* wyp = swy + ry;
         const T* wzp = swz + rz;
-        while (msk) {
-            const int j = __ffs(msk) - 1;
+        // software-pipelined: the next point's shared loads are issued before the
+        // current point's FMAs (two register sets, A / B, alternate)
+        if (msk) {
+            PtLoad<V, T, W, R> a, b;
+            int ja = __ffs(msk) - 1;
             msk &= msk - 1;
-            const T wyv = wyp[j * kYS];
-            T f[R];
-#pragma unroll
-            for (int r = 0; r < R; ++r) f[r] = wyv * wzp[j * ZS + 4 * r];
-            fma_rows<V, T, W, D, R>(acc, sb + j * W, f);
+            a.load(ja, sb, wyp, wzp, ZS);
+            for (;;) {
+                const bool hb = msk != 0;
+                const int jb = hb ? __ffs(msk) - 1 : ja;
+                msk &= msk - 1;
+                b.load(jb, sb, wyp, wzp, ZS);
+                a.apply<D>(acc);
+                if (!hb) break;
+                const bool ha = msk != 0;
+                ja = ha ? __ffs(msk) - 1 : jb;
+                msk &= msk - 1;
+                a.load(ja, sb, wyp, wzp, ZS);
+                b.apply<D>(acc);
+                if (!ha) break;
+            }
         }
         run_points<V, T, W, GX, D + 1, R, ZS>(acc, dmask, run, sb, swy, swz, ry, rz);
     }
