@@ -1,0 +1,8 @@
+mkdir -p gpurun_out
+export NCCL_DEBUG=WARN
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29511 tests/dist_check.py > gpurun_out/r2w_dist_check.log 2>&1
+echo "dist_check rc=$?" >> gpurun_out/r2w_dist_check.log
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29512 tests/dist_pif_check.py > gpurun_out/r2w_dist_pif.log 2>&1
+echo "dist_pif rc=$?" >> gpurun_out/r2w_dist_pif.log
+timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29513 bench.py --gpus 4 --steps 5 --warmup 3 > gpurun_out/r2w_bench2.json 2> gpurun_out/r2w_bench2.err
+echo "bench2 rc=$?" >> gpurun_out/r2w_bench2.err
