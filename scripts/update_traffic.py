@@ -31,6 +31,9 @@ for r in rows[2:]:
     if kind is None:
         continue
     b = float(r[rd].replace(",", "")) * scale[units[rd]] + float(r[wr].replace(",", "")) * scale[units[wr]]
+    if b != b:  # ncu reported nan for this launch
+        print(cfg, kind, "nan (not recorded)", name[:60])
+        continue
     t[cfg][kind] = {"bytes": int(b), "src_sha": sha, "kernel": name.split("(")[0][:80]}
     print(cfg, kind, f"{b / 1e9:.2f} GB", name[:60])
 t["_source"] = ("ncu --set full --clock-control none: dram__bytes_read.sum + dram__bytes_write.sum "
