@@ -672,7 +672,8 @@ __device__ __forceinline__ void run_gather_slots(const Cell (&blk)[NCOMP][R][kBl
                                                  const unsigned (&dmask)[GX], unsigned run,
                                                  const T* swx, const T* swy, const T* swz,
                                                  const uint32_t* sperm, T* red, int* sj, int& cnt,
-                                                 int lane, int ry, int rz, const Out& out) {
+                                                 int lane, int ry, int rz, int cole, int colo,
+                                                 const Out& out) {
     if constexpr (D < GX) {
         unsigned msk = dmask[D] & run;
         // two points per step: both points' shared loads and row-sum chains are
@@ -697,7 +698,8 @@ __device__ __forceinline__ void run_gather_slots(const Cell (&blk)[NCOMP][R][kBl
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
                 if (u == 1 && !two) break;
-                T* e = red + (size_t)(cnt * 32 + red_col(cnt, lane)) * NC;
+                // red_col(cnt, lane) depends on cnt only through its parity
+                T* e = red + (size_t)(cnt * 32 + ((cnt & 1) ? colo : cole)) * NC;
 #pragma unroll
                 for (int m = 0; m < NC; ++m) e[m] = u ? v1[m] : v0[m];
                 if (lane == 0) sj[cnt] = u ? j1 : j0;
@@ -710,7 +712,7 @@ __device__ __forceinline__ void run_gather_slots(const Cell (&blk)[NCOMP][R][kBl
             }
         }
         run_gather_slots<T, Cell, NCOMP, NC, W, GX, D + 1, R, ZS, Out>(
-            blk, dmask, run, swx, swy, swz, sperm, red, sj, cnt, lane, ry, rz, out);
+            blk, dmask, run, swx, swy, swz, sperm, red, sj, cnt, lane, ry, rz, cole, colo, out);
     }
 }
 
@@ -752,6 +754,7 @@ __global__ void __launch_bounds__(32 * NW, (SubGeom<W>::R == 2 ? MINW : (MINW * 
     const uint32_t wbeg = beg + (uint32_t)(((uint64_t)n * warp) / NW);
     const uint32_t wend = beg + (uint32_t)(((uint64_t)n * (warp + 1)) / NW);
     const int ry = lane & 7, rz = lane >> 3;
+    const int cole = red_col(0, lane), colo = red_col(1, lane);
     int cur = -1, cnt = 0;
     Cell blk[NCOMP][R][kBlk];
 
@@ -820,7 +823,7 @@ __global__ void __launch_bounds__(32 * NW, (SubGeom<W>::R == 2 ? MINW : (MINW * 
             }
             const unsigned run = __ballot_sync(0xffffffffu, my_sub == sub);
             run_gather_slots<T, Cell, NCOMP, NC, W, GX, 0, R, ZS, Out>(
-                blk, dmask, run, swx, swy, swz, sperm, red, sj, cnt, lane, ry, rz, out);
+                blk, dmask, run, swx, swy, swz, sperm, red, sj, cnt, lane, ry, rz, cole, colo, out);
             j += __popc(run);
         }
         if (cnt) {  // the batch's last, partial group of slots (sperm is per batch)

@@ -28,6 +28,30 @@ constexpr int kScanTile = kScanThreads * kScanItems;  // counts per scan tile
 
 constexpr int kScatterILP = 4;  // points per thread per scatter round
 
+// L2 residency of setpts: the per-point streams (coordinates, bin_of / rank_of)
+// are read or written once, so they go with the streaming / evict-first hints,
+// while the key arrays (count, offset_key: 4 B per key, 68 MB at C4) -- hit at
+// random by every point -- are accessed under an evict-last policy, so the
+// coordinate stream does not push them out of L2 between two hits.
+__device__ __forceinline__ uint64_t l2_evict_last() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint32_t atomic_add_keep(uint32_t* a, uint32_t v, uint64_t pol) {
+    uint32_t r;
+    asm volatile("atom.global.add.L2::cache_hint.u32 %0, [%1], %2, %3;"
+                 : "=r"(r)
+                 : "l"(a), "r"(v), "l"(pol)
+                 : "memory");
+    return r;
+}
+__device__ __forceinline__ uint32_t ld_keep(const uint32_t* a, uint64_t pol) {
+    uint32_t r;
+    asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(a), "l"(pol));
+    return r;
+}
+
 // Fold onto [0, L) and rescale to fine-grid units (reading R10), fp64.  For x in
 // [0, L) the quotient x / L rounds to at most 1 - 2^-53, so floor(x / L) = 0 and
 // the fold is the identity: the fp64 division runs only for x outside [0, L).
@@ -109,6 +133,7 @@ __global__ void __launch_bounds__(kSortThreads) bin_count_kernel(
     const T* __restrict__ z, uint32_t* __restrict__ count, uint32_t* __restrict__ bin_of,
     uint32_t* __restrict__ rank_of) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const uint64_t keep = l2_evict_last();
     for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < Np;
          i0 += kScatterILP * stride) {
         T xv[kScatterILP], yv[kScatterILP], zv[kScatterILP];
@@ -116,9 +141,9 @@ __global__ void __launch_bounds__(kSortThreads) bin_count_kernel(
         for (int u = 0; u < kScatterILP; ++u) {
             const int64_t i = i0 + u * stride;
             const bool ok = i < Np;
-            xv[u] = ok ? x[i] : (T)0;
-            yv[u] = ok ? y[i] : (T)0;
-            zv[u] = ok ? z[i] : (T)0;
+            xv[u] = ok ? __ldcs(x + i) : (T)0;
+            yv[u] = ok ? __ldcs(y + i) : (T)0;
+            zv[u] = ok ? __ldcs(z + i) : (T)0;
         }
         uint32_t key[kScatterILP], rank[kScatterILP];
 #pragma unroll
@@ -129,13 +154,13 @@ __global__ void __launch_bounds__(kSortThreads) bin_count_kernel(
         // 16.5 ms without it; collisions inside a warp are rare at ~1e4-1e5 bins.)
 #pragma unroll
         for (int u = 0; u < kScatterILP; ++u)
-            if (i0 + u * stride < Np) rank[u] = atomicAdd(&count[key[u]], 1u);
+            if (i0 + u * stride < Np) rank[u] = atomic_add_keep(&count[key[u]], 1u, keep);
 #pragma unroll
         for (int u = 0; u < kScatterILP; ++u) {
             const int64_t i = i0 + u * stride;
             if (i < Np) {
-                bin_of[i] = key[u];
-                rank_of[i] = rank[u];
+                __stcs(bin_of + i, key[u]);
+                __stcs(rank_of + i, rank[u]);
             }
         }
     }
@@ -237,24 +262,26 @@ __global__ void __launch_bounds__(kSortThreads) scatter_kernel(
     // kScatterILP points per thread per round, every load issued before any use:
     // the dependent offset[bin] lookups and the random stores overlap across points
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const uint64_t keep = l2_evict_last();
     for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < Np;
          i0 += kScatterILP * stride) {
-        uint32_t slot[kScatterILP];
+        uint32_t slot[kScatterILP], rk[kScatterILP];
         T xv[kScatterILP], yv[kScatterILP], zv[kScatterILP];
 #pragma unroll
         for (int u = 0; u < kScatterILP; ++u) {
             const int64_t i = i0 + u * stride;
             const bool ok = i < Np;
-            slot[u] = ok ? bin_of[i] : 0u;
-            xv[u] = ok ? x[i] : (T)0;
-            yv[u] = ok ? y[i] : (T)0;
-            zv[u] = ok ? z[i] : (T)0;
+            slot[u] = ok ? __ldcs(bin_of + i) : 0u;
+            rk[u] = ok ? __ldcs(rank_of + i) : 0u;
+            xv[u] = ok ? __ldcs(x + i) : (T)0;
+            yv[u] = ok ? __ldcs(y + i) : (T)0;
+            zv[u] = ok ? __ldcs(z + i) : (T)0;
         }
 #pragma unroll
         for (int u = 0; u < kScatterILP; ++u) {
             const int64_t i = i0 + u * stride;
             if (i < Np) {
-                slot[u] = offset[slot[u]] + rank_of[i];
+                slot[u] = ld_keep(offset + slot[u], keep) + rk[u];
                 NUFFT_CHECK(slot[u] < (uint32_t)Np);
             }
         }
