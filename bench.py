@@ -164,10 +164,7 @@ def make_inputs(cfg, rank, ws, device, mode_block=None):
     rdt = torch.float64 if cfg["prec"] == "f64" else torch.float32
     cdt = torch.complex128 if cfg["prec"] == "f64" else torch.complex64
     Np = cfg["Np"]
-    if cfg["kind"] == "landau":
-        pts = synthetic.landau_points(Np, seed=1, device=device, dtype=rdt)
-    else:
-        pts = synthetic.uniform_points(Np, seed=1, device=device, dtype=rdt)
+    pts = gen_points(cfg, Np, device, rdt)
     c = synthetic.strengths(Np, seed=2, device=device, dtype=cdt)
     if ws > 1:
         L = cfg.get("L", 2 * math.pi)
@@ -346,8 +343,7 @@ def run_ours(args, cfg):
                          points_owned=False, L=cfg.get("L", 2 * math.pi))
         import synthetic
         rdt = torch.float64 if cfg["prec"] == "f64" else torch.float32
-        gen = synthetic.landau_points if cfg["kind"] == "landau" else synthetic.uniform_points
-        allp = gen(Np_total, seed=1, device=device, dtype=rdt)
+        allp = gen_points(cfg, Np_total, device, rdt)
         rr = tuple(a[rank::ws].contiguous() for a in allp)
         del allp
         torch.cuda.empty_cache()
@@ -492,12 +488,22 @@ def ref_sample(cfg):
                                  f"per mode), eps={cfg['eps']:g}")
 
 
-def sample_inputs(cfg, smp):
+def gen_points(cfg, Np, device, rdt):
+    """The config's point distribution (seeded, synthetic/): Landau-perturbed,
+    uniform, or -- with --points clustered -- Gaussian blobs (a setpts contention and
+    load-imbalance stress case, not a paper workload)."""
     import synthetic
     if cfg["kind"] == "landau":
-        x, y, z = (v.numpy() for v in synthetic.landau_points(smp["Np"]))
-    else:
-        x, y, z = (v.numpy() for v in synthetic.uniform_points(smp["Np"]))
+        return synthetic.landau_points(Np, seed=1, device=device, dtype=rdt)
+    if cfg["kind"] == "clustered":
+        return synthetic.clustered_points(Np, L=cfg.get("L", 2 * math.pi), device=device,
+                                          dtype=rdt)
+    return synthetic.uniform_points(Np, seed=1, device=device, dtype=rdt)
+
+
+def sample_inputs(cfg, smp):
+    import synthetic
+    x, y, z = (v.numpy() for v in gen_points(cfg, smp["Np"], "cpu", torch.float64))
     c = synthetic.strengths(smp["Np"]).numpy()
     fk = synthetic.modes(*smp["N"]).numpy()
     return x, y, z, c, fk
@@ -744,6 +750,8 @@ def main():
                     help="1: the paper's pruned sigma = 2 FFT (eight N^3 parity sub-grid FFTs)")
     ap.add_argument("--interp-method", type=int, default=0,
                     help="ablation: 1 / 2 = the paper's Direct Interpolation, caller / sorted order")
+    ap.add_argument("--points", default=None, choices=["clustered"],
+                    help="NUFFT configs: replace the config's point distribution (stress case)")
     ap.add_argument("--real", action="store_true",
                     help="NUFFT configs: real strengths / outputs (R2C / C2R transforms)")
     args = ap.parse_args()
@@ -753,6 +761,8 @@ def main():
     if args.warmup < 3:
         args.warmup = 3
     cfg = CONFIGS[args.config]
+    if args.points and cfg["kind"] != "pif":
+        cfg = dict(cfg, kind=args.points)
     if args.impl == "reference":
         out = run_reference(args, cfg)
     elif cfg["kind"] == "pif":
